@@ -1,0 +1,151 @@
+/*
+ * ndg.h -- C ABI of libndg.so, the B200 (sm_100a) kernels of the culled N-D Gaussian-mixture hot path.
+ *
+ * This library takes the slot of the reference's compiled inner-loop module `ndgauss.kernels._core`
+ * (/root/reference/pkg/setup.py:32-53: Cython -> C + OpenMP, selected at import time, source absent)
+ * behind the reference package's module-level operations. The
+ * reference never published `_core`'s signatures, so each entry point below names the SPEC
+ * operation it replaces; INTEGRATION.md shows the ctypes binding `ndgauss/kernels/__init__.py`
+ * would add.
+ *
+ * Conventions (all entry points):
+ *   - Every pointer is a DEVICE pointer owned by the caller (PyTorch tensors in the Python host).
+ *     The library never allocates device memory; sizes come from ndg_*_floats / _doubles below.
+ *   - `stream` is a cudaStream_t; work is enqueued on it and the call returns without syncing.
+ *   - Return value: NDG_OK (0) or a negative launch/argument error (see ndg_last_error()).
+ *     Data errors (non-finite raw parameters, non-finite gradients) are written to the device
+ *     `ndg_status` and read back by the host once per step; they map 1:1 onto the reference's
+ *     exception classes InvalidParameterError / NonFiniteGradientError
+ *     (/root/reference/pkg/src/ndgauss/errors.py:8-33).
+ *   - Layouts (row-major, float32 unless noted):
+ *       raw component row  : mean_raw[N] | chol_raw[P] | color_raw[3] | amp_raw[1]   (
+ *                            chol_raw is the row-major lower packing of SPEC.md:31, P = N(N+1)/2)
+ *       raw child row      : rel_mean_raw[N] | rel_chol_raw[P] | color_raw[3] | amp_raw
+ *       component flags    : uint8, bit0 = has live child, bit1 = frozen
+ *       evaluated index e  : e < G is parent e; G <= e < 2G is the child of component e - G
+ *       projection vectors : float64 [k][N]
+ *       projected bounds   : float64 [k][Gev]; tile bounds float64 [T][k]
+ *       candidate lists    : CSR, offsets int64 [T+1], indices int32 ascending per tile
+ *   - Supported N: 1..16 (ndg_supported_dims). Tile size: 1..1024 queries.
+ */
+#ifndef NDG_H
+#define NDG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NDG_ABI_VERSION 1
+
+enum ndg_error {
+    NDG_OK = 0,
+    NDG_ERR_INVALID_PARAMETER = 1,    /* data error: non-finite raw parameter       */
+    NDG_ERR_NONFINITE_GRADIENT = 2,   /* data error: non-finite gradient           */
+    NDG_ERR_BAD_ARGUMENT = -1,        /* launch error: invalid sizes / pointers                  */
+    NDG_ERR_UNSUPPORTED_DIMS = -2,    /* launch error: N outside 1..16                           */
+    NDG_ERR_CUDA = -3                 /* launch error: CUDA runtime failure                      */
+};
+
+enum ndg_block { NDG_BLOCK_MEAN = 0, NDG_BLOCK_CHOL = 1, NDG_BLOCK_COLOR = 2, NDG_BLOCK_AMP = 3 };
+enum ndg_amp_mode { NDG_BRIGHTNESS = 0, NDG_OPACITY = 1 };
+
+/*
+ * Device-side status word (zero-initialised by the caller before a step). Offenders are recorded
+ * deterministically as the lowest key = which * G * R + component * R + entry (which: 0 parent row,
+ * 1 child row; R = ndg_raw_floats(N)), stored as INT64_MAX - key (0 = no error) so that an atomicMax
+ * on zero-initialised memory keeps the lowest key. The host decodes component / block / entry.
+ */
+typedef struct ndg_status {
+    int64_t invalid_key;    /* non-finite raw parameter -> InvalidParameterError      */
+    int64_t nonfinite_key;  /* non-finite gradient     -> NonFiniteGradientError     */
+    int64_t n_degenerate;   /* live Gaussians flagged degenerate this step       */
+    int64_t reserved;
+} ndg_status;
+
+int ndg_abi_version(void);
+const char* ndg_last_error(void);
+int ndg_supported_dims(int n);
+int ndg_raw_floats(int n);        /* N + P + 4                                       */
+int ndg_record_floats(int n);     /* evaluation record stride (float32, 16-B multiple) */
+int ndg_query_floats(int n);      /* backward query record stride: x[N] | dpred[3] | ell */
+int ndg_accum_doubles(int n);     /* accumulator stride: S[P] | t[N] | gA[3] | stats[3] */
+int ndg_num_stats(void);          /* density-control statistics per evaluated Gaussian (3) */
+int ndg_backward_chunk(void);     /* candidates per backward work item (chunk_offsets unit) */
+
+/*
+ * K1 prologue. Replaces activate_cholesky + compose_child + the colour/amplitude activations
+ * (SPEC.md:63-71, 93-101, 86). Writes per evaluated Gaussian the float32 evaluation record,
+ * the float64 mean and packed lower factor (composed for children), and eflags
+ * (bit0 live, bit1 degenerate). Non-finite raw values -> status INVALID_PARAMETER.
+ */
+int ndg_prologue(int n, int64_t G, int64_t Gev, int amp_mode, const float* params, const float* child,
+                 const uint8_t* flags, float* rec, double* mean64, double* chol64, uint8_t* eflags,
+                 ndg_status* status, void* stream);
+
+/* K2 projected bounds. Replaces project_components: m_r = m.r, s_r = ||L^T r||
+ * (FP64, sequential, no FMA); thr = multiplier * s_r, or -1 for non-live Gaussians. */
+int ndg_project(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
+                const double* dirs, int k, double multiplier, double* m_r, double* s_r, double* thr, void* stream);
+
+/* K3 tile bounds. Replaces TileBounds construction. */
+int ndg_tile_bounds(int n, int64_t B, int tile, const float* queries, const double* dirs, int k, double* lo,
+                    double* hi, void* stream);
+
+/* K4a binning, phase 1. cull_tile for every tile: bit-mask [T][ceil(Gev/32)]
+ * of kept candidates (warp ballot) and counts[T] (must be zeroed by the caller). */
+int ndg_cull_mask(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* m_r,
+                  const double* thr, uint32_t* mask, int64_t* counts, void* stream);
+
+/* K4b exclusive scan of counts -> offsets[T+1] and backward work-item offsets[T+1]
+ * (ceil(count / ndg_backward_chunk()) per tile). */
+int ndg_scan_counts(int64_t T, const int64_t* counts, int64_t* offsets, int64_t* chunk_offsets, void* stream);
+
+/* K4c compaction of the mask into ascending CSR indices (prefix scan of popcounts). */
+int ndg_cull_compact(int64_t T, int64_t Gev, const uint32_t* mask, const int64_t* offsets, int32_t* idx,
+                     void* stream);
+
+/*
+ * K5+K6 fused forward + loss. Replaces eval_mixture per query over its tile's candidates
+ * (Eq. 8) and loss_rel_l2. `targets` may be NULL (evaluation only;
+ * qrec and loss_partial are then untouched). With targets: qrec[b] = x | dpred | ell and
+ * loss_partial[t] = sum of the tile's per-query loss shares (float64); n_total is the global batch
+ * size the mean divides by (3 * n_total entries).
+ */
+int ndg_forward(int n, int64_t B, int tile, const float* queries, const float* targets, const float* rec,
+                const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total, float* pred, float* qrec,
+                double* loss_partial, void* stream);
+
+/* Deterministic fixed-order sum of the per-tile loss partials. */
+int ndg_loss_finalize(int64_t T, const double* loss_partial, double* loss, void* stream);
+
+/*
+ * K7 fused backward. Replaces the pair loop of `backward`: per (tile, chunk of
+ * candidates) one thread per Gaussian sweeps the tile's queries and accumulates the sufficient
+ * statistics S, t, gA and the density-control statistics, then adds them to accum[Gev][A]
+ * (float64, zeroed by the caller).
+ */
+int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec, const int64_t* offsets,
+                 const int32_t* idx, const int64_t* chunk_offsets, int64_t n_chunks, double* accum, void* stream);
+
+/*
+ * K8 epilogue. Replaces the tail of `backward`: raw-parameter gradients of parents
+ * and live children including the child->parent cross terms; stats[Gev][3] =
+ * (loss share, gradient proxy, pairs). Non-finite gradients -> status NONFINITE_GRADIENT.
+ */
+int ndg_epilogue(int n, int64_t G, int64_t Gev, int amp_mode, const float* params, const float* child,
+                 const uint8_t* flags, const uint8_t* eflags, const double* chol64, const double* accum,
+                 float* grad_params, float* grad_child, float* stats, ndg_status* status, void* stream);
+
+/* K9 Adam. Replaces adam_step with per-block learning rates.
+ * Rows whose row_mask byte is 0 are left untouched (absent children, frozen components). */
+int ndg_adam(int n, int64_t rows, float* params, const float* grad, float* m1, float* m2, const uint8_t* row_mask,
+             int step, float lr_mean, float lr_chol, float lr_color, float lr_amp, float beta1, float beta2,
+             float eps, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NDG_H */

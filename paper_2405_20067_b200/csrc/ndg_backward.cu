@@ -1,0 +1,169 @@
+// K7 fused backward (sm_100a, FP32 pipe, float64 cross-tile reduction).
+//
+// Replaces the pair loop of `backward`. Gaussian-stationary mapping: a work item
+// is (tile, chunk of kBwdChunk candidates); each thread owns one candidate Gaussian, keeps its
+// evaluation record AND all of its accumulators in registers, and sweeps the tile's query records
+// (x | dpred | ell, staged in shared memory by one TMA bulk copy) as warp-uniform LDS.128
+// broadcasts. Per pair, with h = dpred . a and w = g * h:
+//   recompute z~, s~, g                              (as the forward)
+//   S' += (w z~) z~^T (lower),  t' += w z~,  gA += g dpred
+//   loss_share += g * ell,      proxy += |w| sqrt(s~)        (density-control statistics)
+// so the per-query reduction the query-stationary mapping would need (A(N) warp shuffles per pair)
+// disappears; the only reduction is one float64 atomicAdd per accumulator per (tile, candidate),
+// amortised over the tile's queries. The epilogue (ndg_prep.cu) applies the -1/C^2, -1/C scalings.
+#include "ndg_common.cuh"
+
+using namespace ndg;
+
+namespace {
+
+constexpr int kBwdThreads = kBwdChunk;
+
+template <int N>
+__global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? 3 : 1))
+    backward_kernel(int64_t T, int tile, const float* __restrict__ qrec, const float* __restrict__ rec,
+                    const int64_t* __restrict__ offsets, const int32_t* __restrict__ idx,
+                    const int64_t* __restrict__ chunk_off, double* __restrict__ accum) {
+    constexpr int RS = rec_floats(N);
+    constexpr int QS = qrec_floats(N);
+    constexpr int P = n_chol(N);
+    constexpr int A = acc_doubles(N);
+    constexpr int A0 = rec_a(N);
+    extern __shared__ __align__(128) float s_q[];   // [tile][QS]
+    __shared__ __align__(8) uint64_t bar;
+
+    const int tid = threadIdx.x;
+    const int64_t w = blockIdx.x;
+    int64_t lo = 0, hi = T;                      // tile t with chunk_off[t] <= w < chunk_off[t+1]
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (chunk_off[mid] <= w) lo = mid;
+        else hi = mid;
+    }
+    const int64_t t = lo;
+    const int64_t c = offsets[t] + (w - chunk_off[t]) * kBwdChunk + tid;
+    const bool active = c < offsets[t + 1];
+
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const uint32_t bytes = (uint32_t)(tile * QS * 4);
+        mbar_arrive_expect_tx(&bar, bytes);
+        bulk_g2s(s_q, qrec + t * tile * QS, bytes, &bar);
+    }
+
+    float r[RS];
+    int64_t e = 0;
+    if (active) {
+        e = idx[c];
+        const float4* r4 = reinterpret_cast<const float4*>(rec + e * RS);
+#pragma unroll
+        for (int v = 0; v < RS / 4; ++v) {
+            const float4 x = __ldg(r4 + v);
+            r[4 * v] = x.x;
+            r[4 * v + 1] = x.y;
+            r[4 * v + 2] = x.z;
+            r[4 * v + 3] = x.w;
+        }
+    }
+    mbar_wait(&bar, 0);
+    if (!active) return;
+
+    float S[P], tv[N], gA[3], ls = 0.f, px = 0.f;
+#pragma unroll
+    for (int i = 0; i < P; ++i) S[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) tv[i] = 0.f;
+    gA[0] = gA[1] = gA[2] = 0.f;
+
+    for (int q = 0; q < tile; ++q) {
+        float xq[QS];
+        const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
+#pragma unroll
+        for (int v = 0; v < QS / 4; ++v) {
+            const float4 x = q4[v];
+            xq[4 * v] = x.x;
+            xq[4 * v + 1] = x.y;
+            xq[4 * v + 2] = x.z;
+            xq[4 * v + 3] = x.w;
+        }
+        float z[N];
+        float s2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb(N) + i]);
+#pragma unroll
+            for (int k = 0; k < i; ++k) acc = fmaf(r[rec_lu(N) + tri_s(i, k)], z[k], acc);
+            z[i] = acc;
+            s2 = fmaf(acc, acc, s2);
+        }
+        const float g = ex2_neg(s2);
+        const float dp0 = xq[N], dp1 = xq[N + 1], dp2 = xq[N + 2], ell = xq[N + 3];
+        const float h = fmaf(dp2, r[A0 + 2], fmaf(dp1, r[A0 + 1], dp0 * r[A0]));
+        const float wgt = g * h;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const float u = wgt * z[i];
+            tv[i] += u;
+#pragma unroll
+            for (int j = 0; j <= i; ++j) S[tri(i, j)] = fmaf(u, z[j], S[tri(i, j)]);
+        }
+        gA[0] = fmaf(g, dp0, gA[0]);
+        gA[1] = fmaf(g, dp1, gA[1]);
+        gA[2] = fmaf(g, dp2, gA[2]);
+        ls = fmaf(g, ell, ls);
+        px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
+    }
+
+    double* out = accum + e * A;
+#pragma unroll
+    for (int i = 0; i < P; ++i) atomicAdd(out + i, (double)S[i]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)tv[i]);
+    atomicAdd(out + P + N, (double)gA[0]);
+    atomicAdd(out + P + N + 1, (double)gA[1]);
+    atomicAdd(out + P + N + 2, (double)gA[2]);
+    atomicAdd(out + P + N + 3, (double)ls);
+    atomicAdd(out + P + N + 4, (double)px);
+    atomicAdd(out + P + N + 5, (double)tile);
+}
+
+template <int N>
+int launch_backward(int64_t B, int tile, const float* qrec, const float* rec, const int64_t* off, const int32_t* idx,
+                    const int64_t* chunk_off, int64_t n_chunks, double* accum, cudaStream_t st) {
+    const int64_t T = B / tile;
+    const size_t smem = sizeof(float) * tile * qrec_floats(N);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(backward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    NDG_REQUIRE(n_chunks <= 0x7fffffffLL, "too many backward work items");
+    backward_kernel<N><<<(unsigned)n_chunks, kBwdThreads, smem, st>>>(T, tile, qrec, rec, off, idx, chunk_off,
+                                                                       accum);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+}  // namespace
+
+extern "C" int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec, const int64_t* offsets,
+                            const int32_t* idx, const int64_t* chunk_offsets, int64_t n_chunks, double* accum,
+                            void* stream) {
+    NDG_REQUIRE(tile >= 1 && tile <= 1024 && B % tile == 0, "tile must be in 1..1024 and divide B");
+    if (B == 0 || n_chunks == 0) return NDG_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    switch (n) {
+#define NDG_CASE(NN) \
+    case NN:         \
+        return launch_backward<NN>(B, tile, qrec, rec, offsets, idx, chunk_offsets, n_chunks, accum, st);
+        NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
+        NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
+#undef NDG_CASE
+        default:
+            return NDG_ERR_UNSUPPORTED_DIMS;
+    }
+}

@@ -1,0 +1,129 @@
+// Shared definitions of the libndg.so kernels (sm_100a). See include/ndg.h for the ABI and
+// DESIGN.md for the data layout in HBM and the roofline of each kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ndg.h"
+
+namespace ndg {
+
+constexpr int NMAX = 16;
+constexpr int kBwdChunk = 128;          // candidates per backward work item (one per thread)
+constexpr int kNumStats = 3;
+
+__host__ __device__ constexpr int n_chol(int n) { return n * (n + 1) / 2; }
+__host__ __device__ constexpr int n_strict(int n) { return n * (n - 1) / 2; }
+__host__ __device__ constexpr int pad4(int x) { return (x + 3) & ~3; }
+__host__ __device__ constexpr int tri(int i, int j) { return i * (i + 1) / 2 + j; }
+__host__ __device__ constexpr int tri_s(int i, int j) { return i * (i - 1) / 2 + j; }    // strict lower
+__host__ __device__ constexpr int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ constexpr int raw_floats(int n) { return n + n_chol(n) + 4; }
+
+// Evaluation record (float32), one per evaluated Gaussian, 16-byte multiple so a record is one
+// cp.async.bulk and a run of LDS.128 broadcasts:
+//   rho[N]   = C / L_ii                 (C = sqrt(0.5 * log2 e): folds the -1/2 and ln->log2)
+//   nb[N]    = -C * m_i / L_ii
+//   nlu[S]   = -L_ij / L_ii, strict lower, row-major (S = N(N-1)/2)
+//   a[3]     = alpha * sigmoid(color)   (premultiplied colour)
+// so z~_i = fma(rho_i, x_i, nb_i) + sum_j nlu_ij z~_j equals C * z_i of L z = x - m
+// and g = exp2(-|z~|^2) = exp(-|z|^2 / 2).
+__host__ __device__ constexpr int rec_rho(int) { return 0; }
+__host__ __device__ constexpr int rec_nb(int n) { return n; }
+__host__ __device__ constexpr int rec_lu(int n) { return 2 * n; }
+__host__ __device__ constexpr int rec_a(int n) { return 2 * n + n_strict(n); }
+__host__ __device__ constexpr int rec_floats(int n) { return pad4(2 * n + n_strict(n) + 3); }
+
+// Backward query record (float32): x[N] | dpred[3] | ell, produced by the fused forward+loss.
+__host__ __device__ constexpr int qrec_floats(int n) { return pad4(n + 4); }
+
+// Accumulators per evaluated Gaussian (float64): S'[P] | t'[N] | gA[3] | loss_share | proxy | pairs
+// in the scaled z~ units with coefficient +g*h (the epilogue applies -1/C^2, -1/C, 1/C).
+__host__ __device__ constexpr int acc_doubles(int n) { return n_chol(n) + n + 3 + kNumStats; }
+
+constexpr double kC = 0.84932180028801907;      // sqrt(0.5 * log2(e))
+
+}  // namespace ndg
+
+// error string (per-thread) defined in ndg_prep.cu
+extern "C" void ndg_set_last_error(const char* msg);
+
+#define NDG_CHECK_LAUNCH()                                                  \
+    do {                                                                    \
+        cudaError_t e_ = cudaGetLastError();                                \
+        if (e_ != cudaSuccess) {                                            \
+            ndg_set_last_error(cudaGetErrorString(e_));                     \
+            return NDG_ERR_CUDA;                                            \
+        }                                                                   \
+    } while (0)
+
+#define NDG_REQUIRE(cond, msg)                                              \
+    do {                                                                    \
+        if (!(cond)) {                                                      \
+            ndg_set_last_error(msg);                                        \
+            return NDG_ERR_BAD_ARGUMENT;                                    \
+        }                                                                   \
+    } while (0)
+
+// ---------------------------------------------------------------------------------------------
+// PTX helpers: mbarrier + 1-D bulk copy (TMA engine), fast exp2 / sqrt.
+// ---------------------------------------------------------------------------------------------
+namespace ndg {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk copy global -> shared through the TMA engine, completing bytes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ float ex2_neg(float s) {   // 2^(-s), MUFU.EX2 (ftz)
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-s));
+    return r;
+}
+
+__device__ __forceinline__ float sqrt_approx(float s) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
+    return r;
+}
+
+}  // namespace ndg

@@ -1,0 +1,192 @@
+// K5+K6 fused forward + loss (sm_100a, FP32 pipe).
+//
+// Replaces eval_mixture at every query over its tile's candidate list (Eq. 8,
+// PAPER.md:368-371) plus loss_rel_l2. Query-stationary mapping: one CTA per tile,
+// each thread owns kQPT queries in registers; the tile's candidate records are streamed through a
+// double-buffered shared-memory ring, each record brought in by one 1-D bulk copy on the TMA engine
+// (cp.async.bulk + mbarrier complete_tx), and read back as warp-uniform LDS.128 broadcasts. Per pair:
+//   z~_i = fma(rho_i, x_i, nb_i) + sum_{j<i} nlu_ij z~_j      (forward substitution)
+//   s~ = |z~|^2,  g = ex2(-s~) = exp(-|z|^2/2),  pred += g * a
+// i.e. N + N(N-1)/2 + N FFMA, one MUFU.EX2 and 3 FFMA: the whole per-pair cost is FP32-pipe issue.
+// When targets are given the CTA finishes the tile with the relative-L2 loss: dpred, each query's
+// loss share, the backward query record (x | dpred | ell) and a per-tile float64 loss partial.
+#include "ndg_common.cuh"
+
+using namespace ndg;
+
+namespace {
+
+constexpr int kFwdThreads = 128;
+constexpr int kQPT = 2;                     // queries per thread -> 256 queries per pass
+constexpr int kChunk = 32;                  // candidate records per ring stage (one per lane of warp 0)
+constexpr int kStages = 2;
+
+template <int N>
+__global__ void __launch_bounds__(kFwdThreads, 4)
+    forward_kernel(int tile, const float* __restrict__ queries, const float* __restrict__ targets,
+                   const float* __restrict__ rec, const int64_t* __restrict__ offsets,
+                   const int32_t* __restrict__ idx, float eps, double inv3n, float* __restrict__ pred,
+                   float* __restrict__ qrec, double* __restrict__ loss_partial) {
+    constexpr int RS = rec_floats(N);
+    constexpr int QS = qrec_floats(N);
+    constexpr int A0 = rec_a(N);
+    extern __shared__ __align__(128) float s_rec[];           // [kStages][kChunk][RS]
+    __shared__ __align__(8) uint64_t full_bar[kStages];
+    __shared__ double s_loss[kFwdThreads / 32];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t t = blockIdx.x;
+    const int64_t beg = offsets[t], end = offsets[t + 1];
+    const int nchunks = (int)((end - beg + kChunk - 1) / kChunk);
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // producer: warp 0, lane l copies candidate l of chunk c into stage s
+    auto issue = [&](int c, int s) {
+        const int64_t cb = beg + (int64_t)c * kChunk;
+        const int n_in = (int)imin64(kChunk, end - cb);
+        if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(n_in * RS * 4));
+        __syncwarp();
+        if (lane < n_in) {
+            const int64_t e = idx[cb + lane];
+            bulk_g2s(s_rec + (s * kChunk + lane) * RS, rec + e * RS, RS * 4, &full_bar[s]);
+        }
+    };
+
+    double loss_acc = 0.0;
+    uint32_t phase_ctr = 0;   // ring position across passes (barrier parity bookkeeping)
+    for (int q0 = 0; q0 < tile; q0 += kFwdThreads * kQPT) {
+        float x[kQPT][N], p[kQPT][3];
+        bool valid[kQPT];
+#pragma unroll
+        for (int j = 0; j < kQPT; ++j) {
+            const int qi = q0 + tid + j * kFwdThreads;
+            valid[j] = qi < tile;
+            const float* src = queries + (t * tile + qi) * N;
+#pragma unroll
+            for (int d = 0; d < N; ++d) x[j][d] = valid[j] ? src[d] : 0.f;
+            p[j][0] = p[j][1] = p[j][2] = 0.f;
+        }
+        if (warp == 0) {
+            for (int c = 0; c < kStages && c < nchunks; ++c) issue(c, (int)((phase_ctr + c) % kStages));
+        }
+        for (int c = 0; c < nchunks; ++c) {
+            const uint32_t pos = phase_ctr + c;
+            const int s = (int)(pos % kStages);
+            mbar_wait(&full_bar[s], (pos / kStages) & 1);
+            const int n_in = (int)imin64(kChunk, end - beg - (int64_t)c * kChunk);
+            const float* sr = s_rec + s * kChunk * RS;
+            for (int ci = 0; ci < n_in; ++ci) {
+                float r[RS];
+                const float4* r4 = reinterpret_cast<const float4*>(sr + ci * RS);
+#pragma unroll
+                for (int v = 0; v < RS / 4; ++v) {
+                    const float4 w = r4[v];
+                    r[4 * v] = w.x;
+                    r[4 * v + 1] = w.y;
+                    r[4 * v + 2] = w.z;
+                    r[4 * v + 3] = w.w;
+                }
+#pragma unroll
+                for (int j = 0; j < kQPT; ++j) {
+                    float z[N];
+                    float s2 = 0.f;
+#pragma unroll
+                    for (int i = 0; i < N; ++i) {
+                        float acc = fmaf(r[rec_rho(N) + i], x[j][i], r[rec_nb(N) + i]);
+#pragma unroll
+                        for (int k = 0; k < i; ++k) acc = fmaf(r[rec_lu(N) + tri_s(i, k)], z[k], acc);
+                        z[i] = acc;
+                        s2 = fmaf(acc, acc, s2);
+                    }
+                    const float g = ex2_neg(s2);
+                    p[j][0] = fmaf(g, r[A0], p[j][0]);
+                    p[j][1] = fmaf(g, r[A0 + 1], p[j][1]);
+                    p[j][2] = fmaf(g, r[A0 + 2], p[j][2]);
+                }
+            }
+            __syncthreads();   // every warp is done with stage s
+            if (warp == 0 && c + kStages < nchunks) issue(c + kStages, s);
+        }
+        phase_ctr += (uint32_t)nchunks;
+
+#pragma unroll
+        for (int j = 0; j < kQPT; ++j) {
+            if (!valid[j]) continue;
+            const int64_t b = t * tile + q0 + tid + j * kFwdThreads;
+            pred[b * 3] = p[j][0];
+            pred[b * 3 + 1] = p[j][1];
+            pred[b * 3 + 2] = p[j][2];
+            if (targets) {
+                float* qr = qrec + b * QS;
+                double ell = 0.0;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    const double pv = p[j][ch], dv = pv - (double)targets[b * 3 + ch], den = pv * pv + (double)eps;
+                    ell += dv * dv / den;
+                    qr[N + ch] = (float)(2.0 * dv / den * inv3n);
+                }
+                ell *= inv3n;
+#pragma unroll
+                for (int d = 0; d < N; ++d) qr[d] = x[j][d];
+                qr[N + 3] = (float)ell;
+#pragma unroll
+                for (int d = N + 4; d < QS; ++d) qr[d] = 0.f;
+                loss_acc += ell;
+            }
+        }
+    }
+    if (targets) {   // fixed-order block reduction -> per-tile partial (deterministic)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
+        if (lane == 0) s_loss[warp] = loss_acc;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int w = 0; w < kFwdThreads / 32; ++w) s += s_loss[w];
+            loss_partial[t] = s;
+        }
+    }
+}
+
+template <int N>
+int launch_forward(int64_t B, int tile, const float* q, const float* tgt, const float* rec, const int64_t* off,
+                   const int32_t* idx, float eps, int64_t n_total, float* pred, float* qrec, double* lp,
+                   cudaStream_t st) {
+    const int64_t T = B / tile;
+    const size_t smem = sizeof(float) * kStages * kChunk * rec_floats(N);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(forward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    forward_kernel<N><<<(unsigned)T, kFwdThreads, smem, st>>>(tile, q, tgt, rec, off, idx, eps,
+                                                              1.0 / (3.0 * (double)n_total), pred, qrec, lp);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+}  // namespace
+
+extern "C" int ndg_forward(int n, int64_t B, int tile, const float* queries, const float* targets, const float* rec,
+                           const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total, float* pred,
+                           float* qrec, double* loss_partial, void* stream) {
+    NDG_REQUIRE(tile >= 1 && tile <= 1024 && B % tile == 0, "tile must be in 1..1024 and divide B");
+    NDG_REQUIRE(!targets || (qrec && loss_partial && n_total > 0), "targets need qrec, loss_partial, n_total");
+    if (B == 0) return NDG_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    switch (n) {
+#define NDG_CASE(NN) \
+    case NN:         \
+        return launch_forward<NN>(B, tile, queries, targets, rec, offsets, idx, eps, n_total, pred, qrec, loss_partial, st);
+        NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
+        NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
+#undef NDG_CASE
+        default:
+            return NDG_ERR_UNSUPPORTED_DIMS;
+    }
+}

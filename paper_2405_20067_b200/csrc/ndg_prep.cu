@@ -1,0 +1,618 @@
+// libndg.so: prologue (K1), projected bounds (K2), tile bounds (K3), binning (K4a-c), loss
+// finalisation, epilogue (K8) and Adam (K9). The FP32 pair kernels K5 / K7 live in ndg_forward.cu /
+// ndg_backward.cu. Reference operations are cited per kernel (SPEC.md = /root/reference/SPEC.md).
+//
+// Bit-exactness of the culling path: every float64 sum below runs in the oracle's order with
+// explicit __dmul_rn / __dadd_rn (no FMA contraction), so m_r, s_r, the tile bounds and therefore
+// the candidate lists equal oracle/ndg_oracle.py's bit for bit given the same activated factors.
+#include <climits>
+#include <cstdio>
+#include <cstring>
+
+#include "ndg_common.cuh"
+
+using namespace ndg;
+
+static thread_local char g_last_error[256] = "";
+
+extern "C" void ndg_set_last_error(const char* msg) {
+    std::strncpy(g_last_error, msg, sizeof(g_last_error) - 1);
+    g_last_error[sizeof(g_last_error) - 1] = 0;
+}
+
+extern "C" const char* ndg_last_error(void) { return g_last_error; }
+extern "C" int ndg_abi_version(void) { return NDG_ABI_VERSION; }
+extern "C" int ndg_supported_dims(int n) { return n >= 1 && n <= NMAX; }
+extern "C" int ndg_raw_floats(int n) { return raw_floats(n); }
+extern "C" int ndg_record_floats(int n) { return rec_floats(n); }
+extern "C" int ndg_query_floats(int n) { return qrec_floats(n); }
+extern "C" int ndg_accum_doubles(int n) { return acc_doubles(n); }
+extern "C" int ndg_num_stats(void) { return kNumStats; }
+extern "C" int ndg_backward_chunk(void) { return kBwdChunk; }
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+__device__ __forceinline__ void record_key(int64_t* slot, int64_t key) {
+    atomicMax(reinterpret_cast<unsigned long long*>(slot), (unsigned long long)(LLONG_MAX - key));
+}
+
+__device__ __forceinline__ double act_offdiag(double r) {   // 2 * sigmoid(r) - 1
+    double s = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-r)));
+    return __dsub_rn(__dmul_rn(2.0, s), 1.0);
+}
+
+__device__ __forceinline__ double sigmoid64(double r) { return 1.0 / (1.0 + exp(-r)); }
+
+// ---------------------------------------------------------------------------------------------
+// K1 prologue: activate_cholesky, compose_child (Eq. 6-7),
+// alpha / colour activation. One thread per evaluated Gaussian.
+// ---------------------------------------------------------------------------------------------
+__global__ void prologue_kernel(int n, int64_t G, int64_t Gev, int amp_mode, const float* __restrict__ params,
+                                const float* __restrict__ child, const uint8_t* __restrict__ flags,
+                                float* __restrict__ rec, double* __restrict__ mean64, double* __restrict__ chol64,
+                                uint8_t* __restrict__ eflags, ndg_status* st) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= Gev) return;
+    const int P = n_chol(n), R = raw_floats(n), RS = rec_floats(n);
+    const bool is_child = e >= G;
+    const int64_t i = is_child ? e - G : e;
+    const uint8_t f = flags ? flags[i] : 0;
+    const bool frozen = f & 2, has_child = f & 1;
+    const float* prow = params + i * R;
+    bool live = !frozen && (!is_child || has_child);
+
+    // non-finite raw parameters -> InvalidParameterError; parent rows always checked,
+    // child rows only when the child is live.
+    if (!is_child || has_child) {
+        const float* row = is_child ? child + i * R : prow;
+        for (int t = 0; t < R; ++t)
+            if (!isfinite(row[t])) {
+                record_key(&st->invalid_key, (is_child ? G * R : 0) + i * R + t);
+                break;
+            }
+    }
+
+    double L[n_chol(NMAX)], m[NMAX];
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c <= r; ++c) {
+            double raw = (double)prow[n + tri(r, c)];
+            L[tri(r, c)] = (r == c) ? exp(raw) : act_offdiag(raw);
+        }
+    for (int r = 0; r < n; ++r) m[r] = (double)prow[r];
+    const float* arow = prow;
+    if (is_child) {
+        const float* crow = child + i * R;
+        double U[n_chol(NMAX)], mc[NMAX], Lc[n_chol(NMAX)];
+        for (int r = 0; r < n; ++r)
+            for (int c = 0; c <= r; ++c) {
+                double raw = (double)crow[n + tri(r, c)];
+                U[tri(r, c)] = (r == c) ? exp(raw) : act_offdiag(raw);
+            }
+        for (int r = 0; r < n; ++r) {   // m_c = L m_u + m_p, ascending k
+            double acc = __dmul_rn(L[tri(r, 0)], (double)crow[0]);
+            for (int k = 1; k <= r; ++k) acc = __dadd_rn(acc, __dmul_rn(L[tri(r, k)], (double)crow[k]));
+            mc[r] = __dadd_rn(acc, m[r]);
+        }
+        for (int r = 0; r < n; ++r)     // L U, ascending k
+            for (int c = 0; c <= r; ++c) {
+                double acc = __dmul_rn(L[tri(r, c)], U[tri(c, c)]);
+                for (int k = c + 1; k <= r; ++k) acc = __dadd_rn(acc, __dmul_rn(L[tri(r, k)], U[tri(k, c)]));
+                Lc[tri(r, c)] = acc;
+            }
+        for (int t = 0; t < P; ++t) L[t] = Lc[t];
+        for (int r = 0; r < n; ++r) m[r] = mc[r];
+        arow = crow;
+    }
+    bool degenerate = false;
+    for (int t = 0; t < P; ++t) degenerate |= !isfinite(L[t]);
+    for (int r = 0; r < n; ++r) degenerate |= L[tri(r, r)] < 1e-30;
+    if (degenerate && live) atomicAdd(reinterpret_cast<unsigned long long*>(&st->n_degenerate), 1ull);
+    live = live && !degenerate;
+
+    for (int t = 0; t < P; ++t) chol64[e * P + t] = L[t];
+    for (int r = 0; r < n; ++r) mean64[e * n + r] = m[r];
+    eflags[e] = (uint8_t)((live ? 1 : 0) | (degenerate ? 2 : 0));
+
+    float* out = rec + e * RS;
+    if (!live) {
+        for (int t = 0; t < RS; ++t) out[t] = 0.f;
+        return;
+    }
+    double ampr = (double)arow[n + P + 3];
+    double alpha = amp_mode == NDG_BRIGHTNESS ? exp(ampr) : sigmoid64(ampr);
+    for (int r = 0; r < n; ++r) {
+        double inv = 1.0 / L[tri(r, r)];
+        out[rec_rho(n) + r] = (float)(kC * inv);
+        out[rec_nb(n) + r] = (float)(-kC * m[r] * inv);
+        for (int c = 0; c < r; ++c) out[rec_lu(n) + tri_s(r, c)] = (float)(-L[tri(r, c)] * inv);
+    }
+    for (int ch = 0; ch < 3; ++ch) out[rec_a(n) + ch] = (float)(alpha * sigmoid64((double)arow[n + P + ch]));
+    for (int t = rec_a(n) + 3; t < RS; ++t) out[t] = 0.f;
+}
+
+extern "C" int ndg_prologue(int n, int64_t G, int64_t Gev, int amp_mode, const float* params, const float* child,
+                            const uint8_t* flags, float* rec, double* mean64, double* chol64, uint8_t* eflags,
+                            ndg_status* status, void* stream) {
+    if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
+    NDG_REQUIRE(G >= 0 && (Gev == G || Gev == 2 * G), "Gev must be G or 2G");
+    NDG_REQUIRE(Gev == G || child != nullptr, "child rows required when Gev == 2G");
+    if (Gev == 0) return NDG_OK;
+    int threads = 128;
+    prologue_kernel<<<(unsigned)((Gev + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+        n, G, Gev, amp_mode, params, child, flags, rec, mean64, chol64, eflags, status);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K2 projected bounds: project_components (Eq. 3-4). FP64, oracle order.
+// ---------------------------------------------------------------------------------------------
+__global__ void project_kernel(int n, int64_t Gev, const double* __restrict__ mean64,
+                               const double* __restrict__ chol64, const uint8_t* __restrict__ eflags,
+                               const double* __restrict__ dirs, int k, double mult, double* __restrict__ m_r,
+                               double* __restrict__ s_r, double* __restrict__ thr) {
+    extern __shared__ double sdir[];
+    for (int t = threadIdx.x; t < k * n; t += blockDim.x) sdir[t] = dirs[t];
+    __syncthreads();
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= Gev) return;
+    const int P = n_chol(n);
+    double m[NMAX], L[n_chol(NMAX)];
+    for (int r = 0; r < n; ++r) m[r] = mean64[e * n + r];
+    for (int t = 0; t < P; ++t) L[t] = chol64[e * P + t];
+    const uint8_t f = eflags[e];
+    const bool live = f & 1, degenerate = f & 2;
+    for (int ri = 0; ri < k; ++ri) {
+        const double* r = sdir + ri * n;
+        double acc = __dmul_rn(m[0], r[0]);
+        for (int j = 1; j < n; ++j) acc = __dadd_rn(acc, __dmul_rn(m[j], r[j]));
+        double ss = 0.0;
+        for (int j = 0; j < n; ++j) {
+            double u = __dmul_rn(L[tri(j, j)], r[j]);           // (L^T r)_j = sum_{i>=j} L_ij r_i
+            for (int i = j + 1; i < n; ++i) u = __dadd_rn(u, __dmul_rn(L[tri(i, j)], r[i]));
+            ss = (j == 0) ? __dmul_rn(u, u) : __dadd_rn(ss, __dmul_rn(u, u));
+        }
+        double s = degenerate ? 0.0 : __dsqrt_rn(ss);
+        m_r[ri * Gev + e] = acc;
+        s_r[ri * Gev + e] = s;
+        thr[ri * Gev + e] = live ? __dmul_rn(mult, s) : -1.0;
+    }
+}
+
+extern "C" int ndg_project(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
+                           const double* dirs, int k, double multiplier, double* m_r, double* s_r, double* thr,
+                           void* stream) {
+    if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
+    NDG_REQUIRE(k >= 1 && k <= 256, "k must be in 1..256");
+    if (Gev == 0) return NDG_OK;
+    int threads = 128;
+    project_kernel<<<(unsigned)((Gev + threads - 1) / threads), threads, sizeof(double) * k * n,
+                     as_stream(stream)>>>(n, Gev, mean64, chol64, eflags, dirs, k, multiplier, m_r, s_r, thr);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K3 tile bounds: TileBounds. One CTA per tile, one thread per query.
+// ---------------------------------------------------------------------------------------------
+__global__ void tile_bounds_kernel(int n, int tile, const float* __restrict__ q, const double* __restrict__ dirs,
+                                   int k, double* __restrict__ lo, double* __restrict__ hi) {
+    __shared__ double s_lo[32], s_hi[32];
+    const int64_t t = blockIdx.x;
+    const int qi = threadIdx.x;
+    const bool valid = qi < tile;
+    float x[NMAX];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) x[j] = (valid && j < n) ? q[(t * tile + qi) * n + j] : 0.f;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (int ri = 0; ri < k; ++ri) {
+        const double* r = dirs + ri * n;
+        double acc = __dmul_rn((double)x[0], r[0]);
+#pragma unroll
+        for (int j = 1; j < NMAX; ++j)
+            if (j < n) acc = __dadd_rn(acc, __dmul_rn((double)x[j], r[j]));
+        double mn = valid ? acc : INFINITY, mx = valid ? acc : -INFINITY;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            s_lo[warp] = mn;
+            s_hi[warp] = mx;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < nwarps; ++w) {
+                mn = fmin(mn, s_lo[w]);
+                mx = fmax(mx, s_hi[w]);
+            }
+            lo[t * k + ri] = mn;
+            hi[t * k + ri] = mx;
+        }
+        __syncthreads();
+    }
+}
+
+extern "C" int ndg_tile_bounds(int n, int64_t B, int tile, const float* queries, const double* dirs, int k,
+                               double* lo, double* hi, void* stream) {
+    if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
+    NDG_REQUIRE(tile >= 1 && tile <= 1024 && B % tile == 0, "tile must be in 1..1024 and divide B");
+    NDG_REQUIRE(k >= 1 && k <= 256, "k must be in 1..256");
+    int64_t T = B / tile;
+    if (T == 0) return NDG_OK;
+    int threads = ((tile + 31) / 32) * 32;
+    tile_bounds_kernel<<<(unsigned)T, threads, 0, as_stream(stream)>>>(n, tile, queries, dirs, k, lo, hi);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K4a cull mask: cull_tile for all tiles. Thread = evaluated Gaussian, CTA =
+// 256 Gaussians x kCullTiles tiles; the Gaussians' (m_r, thr) sit in shared memory, the tiles'
+// intervals are broadcast. Culled iff any vector has lo - m_r > thr or m_r - hi > thr (FP64; the
+// same predicate as max(lo - m_r, m_r - hi, 0) > multiplier * s_r); thr < 0 = never evaluated.
+// Warp ballot -> one mask word per 32 Gaussians; per-CTA popcount -> one atomic per tile.
+// ---------------------------------------------------------------------------------------------
+constexpr int kCullThreads = 256;
+constexpr int kCullTiles = 16;
+
+__global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int k, int64_t Gev,
+                                                                  const double* __restrict__ lo,
+                                                                  const double* __restrict__ hi,
+                                                                  const double* __restrict__ m_r,
+                                                                  const double* __restrict__ thr,
+                                                                  uint32_t* __restrict__ mask,
+                                                                  int64_t* __restrict__ counts) {
+    extern __shared__ double sm[];
+    double* s_m = sm;                              // [k][256]
+    double* s_t = sm + k * kCullThreads;           // [k][256]
+    double* s_lo = s_t + k * kCullThreads;         // [kCullTiles][k]
+    double* s_hi = s_lo + kCullTiles * k;
+    __shared__ int s_cnt[kCullTiles][kCullThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t e = blockIdx.x * (int64_t)kCullThreads + tid;
+    const int64_t t0 = blockIdx.y * (int64_t)kCullTiles;
+    const int ntile = (int)imin64(kCullTiles, T - t0);
+    for (int ri = 0; ri < k; ++ri) {
+        s_m[ri * kCullThreads + tid] = e < Gev ? m_r[ri * Gev + e] : 0.0;
+        s_t[ri * kCullThreads + tid] = e < Gev ? thr[ri * Gev + e] : -1.0;
+    }
+    for (int x = tid; x < ntile * k; x += kCullThreads) {
+        s_lo[x] = lo[t0 * k + x];
+        s_hi[x] = hi[t0 * k + x];
+    }
+    __syncthreads();
+    const bool never = s_t[tid] < 0.0;
+    const int64_t W = (Gev + 31) / 32;
+    for (int tt = 0; tt < ntile; ++tt) {
+        bool kept = !never;
+        for (int ri = 0; ri < k && kept; ++ri) {
+            const double mr = s_m[ri * kCullThreads + tid], th = s_t[ri * kCullThreads + tid];
+            const double l = s_lo[tt * k + ri], h = s_hi[tt * k + ri];
+            if (__dsub_rn(l, mr) > th || __dsub_rn(mr, h) > th) kept = false;
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, kept);
+        if (lane == 0) {
+            const int64_t wi = e >> 5;
+            if (wi < W) mask[(t0 + tt) * W + wi] = word;
+            s_cnt[tt][warp] = __popc(word);
+        }
+    }
+    __syncthreads();
+    if (tid < ntile) {
+        int c = 0;
+        for (int w = 0; w < kCullThreads / 32; ++w) c += s_cnt[tid][w];
+        if (c) atomicAdd(reinterpret_cast<unsigned long long*>(&counts[t0 + tid]), (unsigned long long)c);
+    }
+}
+
+extern "C" int ndg_cull_mask(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* m_r,
+                             const double* thr, uint32_t* mask, int64_t* counts, void* stream) {
+    NDG_REQUIRE(k >= 1 && k <= 64, "k must be in 1..64 for the cull kernel");
+    if (T == 0 || Gev == 0) return NDG_OK;
+    dim3 grid((unsigned)((Gev + kCullThreads - 1) / kCullThreads), (unsigned)((T + kCullTiles - 1) / kCullTiles));
+    NDG_REQUIRE(grid.y <= 65535, "too many tiles for one cull launch");
+    size_t smem = sizeof(double) * (2 * k * kCullThreads + 2 * kCullTiles * k);
+    static thread_local bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(cull_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        attr_set = true;
+    }
+    cull_mask_kernel<<<grid, kCullThreads, smem, as_stream(stream)>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K4b exclusive scan of the per-tile counts (single CTA, chunked Hillis-Steele in shared memory).
+// ---------------------------------------------------------------------------------------------
+__global__ void scan_counts_kernel(int64_t T, const int64_t* __restrict__ counts, int64_t* __restrict__ offsets,
+                                   int64_t* __restrict__ chunk_offsets) {
+    __shared__ int64_t s_a[1024], s_b[1024];
+    __shared__ int64_t carry_a, carry_b;
+    if (threadIdx.x == 0) carry_a = carry_b = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < T; base += 1024) {
+        const int64_t t = base + threadIdx.x;
+        const int64_t c = t < T ? counts[t] : 0;
+        s_a[threadIdx.x] = c;
+        s_b[threadIdx.x] = (c + kBwdChunk - 1) / kBwdChunk;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            int64_t va = threadIdx.x >= o ? s_a[threadIdx.x - o] : 0;
+            int64_t vb = threadIdx.x >= o ? s_b[threadIdx.x - o] : 0;
+            __syncthreads();
+            s_a[threadIdx.x] += va;
+            s_b[threadIdx.x] += vb;
+            __syncthreads();
+        }
+        if (t < T) {   // inclusive -> offsets[t + 1]
+            offsets[t + 1] = carry_a + s_a[threadIdx.x];
+            chunk_offsets[t + 1] = carry_b + s_b[threadIdx.x];
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) {
+            carry_a += s_a[1023];
+            carry_b += s_b[1023];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        offsets[0] = 0;
+        chunk_offsets[0] = 0;
+    }
+}
+
+extern "C" int ndg_scan_counts(int64_t T, const int64_t* counts, int64_t* offsets, int64_t* chunk_offsets,
+                               void* stream) {
+    scan_counts_kernel<<<1, 1024, 0, as_stream(stream)>>>(T, counts, offsets, chunk_offsets);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K4c compaction: CTA per tile; block prefix scan of per-word popcounts, then each thread writes
+// the ascending indices of its word's set bits.
+// ---------------------------------------------------------------------------------------------
+constexpr int kCompactThreads = 256;
+
+__global__ void __launch_bounds__(kCompactThreads) compact_kernel(int64_t Gev, const uint32_t* __restrict__ mask,
+                                                                   const int64_t* __restrict__ offsets,
+                                                                   int32_t* __restrict__ idx) {
+    __shared__ int s_warp[kCompactThreads / 32];
+    __shared__ int64_t s_base;
+    const int64_t t = blockIdx.x;
+    const int64_t W = (Gev + 31) / 32;
+    const uint32_t* row = mask + t * W;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_base = offsets[t];
+    __syncthreads();
+    for (int64_t w0 = 0; w0 < W; w0 += kCompactThreads) {
+        const int64_t wi = w0 + tid;
+        uint32_t word = wi < W ? row[wi] : 0u;
+        int c = __popc(word), incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < kCompactThreads / 32; ++w) {
+            if (w < warp) before += s_warp[w];
+            total += s_warp[w];
+        }
+        int64_t pos = s_base + before + incl - c;
+        while (word) {
+            int b = __ffs(word) - 1;
+            idx[pos++] = (int32_t)(wi * 32 + b);
+            word &= word - 1;
+        }
+        __syncthreads();
+        if (tid == 0) s_base += total;
+        __syncthreads();
+    }
+}
+
+extern "C" int ndg_cull_compact(int64_t T, int64_t Gev, const uint32_t* mask, const int64_t* offsets, int32_t* idx,
+                                void* stream) {
+    if (T == 0 || Gev == 0) return NDG_OK;
+    compact_kernel<<<(unsigned)T, kCompactThreads, 0, as_stream(stream)>>>(Gev, mask, offsets, idx);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Loss finalisation: fixed-order float64 sum of the per-tile partials (deterministic).
+// ---------------------------------------------------------------------------------------------
+__global__ void loss_finalize_kernel(int64_t T, const double* __restrict__ part, double* __restrict__ loss) {
+    __shared__ double s[256];
+    double acc = 0.0;
+    for (int64_t t = threadIdx.x; t < T; t += 256) acc += part[t];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *loss = s[0];
+}
+
+extern "C" int ndg_loss_finalize(int64_t T, const double* loss_partial, double* loss, void* stream) {
+    loss_finalize_kernel<<<1, 256, 0, as_stream(stream)>>>(T, loss_partial, loss);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K8 epilogue: tail of backward. Thread per component; float64.
+//   per evaluated Gaussian: S = -S'/C^2, t = -t'/C; G_L = -tril(L^-T S), dm = -L^-T t
+//   parent: d mean_raw = dm; d chol_raw = G_L * (L_ii | (1 - L_ij^2)/2)
+//   child (L_c = L U, m_c = L m_u + m_p): dU = tril(L^T G_Lc), dm_u = L^T dm_c,
+//          parent += tril(G_Lc U^T) + tril(dm_c m_u^T) on L and dm_c on the mean.
+//   colour / amplitude: d color_raw = gA * alpha * c (1 - c); d amp_raw = (gA . c) * alpha'.
+// ---------------------------------------------------------------------------------------------
+__device__ void solve_upper_t(int n, const double* L, const double* Y, double* X) {   // X = L^-T Y (dense N x N)
+    for (int c = 0; c < n; ++c)
+        for (int i = n - 1; i >= 0; --i) {
+            double acc = Y[i * n + c];
+            for (int k = i + 1; k < n; ++k) acc -= L[tri(k, i)] * X[k * n + c];
+            X[i * n + c] = acc / L[tri(i, i)];
+        }
+}
+
+__global__ void epilogue_kernel(int n, int64_t G, int64_t Gev, int amp_mode, const float* __restrict__ params,
+                                const float* __restrict__ child, const uint8_t* __restrict__ flags,
+                                const uint8_t* __restrict__ eflags, const double* __restrict__ chol64,
+                                const double* __restrict__ accum, float* __restrict__ gp, float* __restrict__ gc,
+                                float* __restrict__ stats, ndg_status* st) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= G) return;
+    const int P = n_chol(n), R = raw_floats(n), A = acc_doubles(n);
+    double GLp[NMAX * NMAX], dmp[NMAX];
+    double S[NMAX * NMAX], X[NMAX * NMAX];
+    for (int t = 0; t < n * n; ++t) GLp[t] = 0.0;
+    for (int r = 0; r < n; ++r) dmp[r] = 0.0;
+    float* op = gp + i * R;
+    float* oc = gc ? gc + i * R : nullptr;
+    for (int t = 0; t < R; ++t) op[t] = 0.f;
+    if (oc)
+        for (int t = 0; t < R; ++t) oc[t] = 0.f;
+    const double* Lp = chol64 + i * P;
+    const double invC = 1.0 / kC, invC2 = invC * invC;
+    const int nev = (Gev == 2 * G) ? 2 : 1;
+    for (int which = 0; which < nev; ++which) {
+        const int64_t e = which ? G + i : i;
+        const double* acc = accum + e * A;
+        float* so = stats + e * kNumStats;
+        if (!(eflags[e] & 1)) {
+            so[0] = so[1] = so[2] = 0.f;
+            continue;
+        }
+        so[0] = (float)acc[P + n + 3];
+        so[1] = (float)(acc[P + n + 4] * invC);
+        so[2] = (float)acc[P + n + 5];
+        const double* Le = chol64 + e * P;
+        for (int r = 0; r < n; ++r)
+            for (int c = 0; c <= r; ++c) S[r * n + c] = S[c * n + r] = -acc[tri(r, c)] * invC2;
+        solve_upper_t(n, Le, S, X);
+        double GL[NMAX * NMAX], dm[NMAX];
+        for (int r = 0; r < n; ++r)
+            for (int c = 0; c < n; ++c) GL[r * n + c] = c <= r ? -X[r * n + c] : 0.0;
+        for (int r = n - 1; r >= 0; --r) {   // dm = -L^-T t (single-column back substitution)
+            double a = -acc[P + r] * invC;
+            for (int k = r + 1; k < n; ++k) a -= Le[tri(k, r)] * dm[k];
+            dm[r] = a / Le[tri(r, r)];
+        }
+        for (int r = 0; r < n; ++r) dm[r] = -dm[r];
+        const float* row = which ? child + i * R : params + i * R;
+        float* out = which ? oc : op;
+        const double ar = (double)row[n + P + 3];
+        const double alpha = amp_mode == NDG_BRIGHTNESS ? exp(ar) : sigmoid64(ar);
+        double dalpha = 0.0;
+        for (int ch = 0; ch < 3; ++ch) {
+            const double cc = sigmoid64((double)row[n + P + ch]);
+            const double gA = acc[P + n + ch];
+            out[n + P + ch] = (float)(gA * alpha * cc * (1.0 - cc));
+            dalpha += gA * cc;
+        }
+        out[n + P + 3] = (float)(dalpha * (amp_mode == NDG_BRIGHTNESS ? alpha : alpha * (1.0 - alpha)));
+        if (!which) {
+            for (int t = 0; t < n * n; ++t) GLp[t] += GL[t];
+            for (int r = 0; r < n; ++r) dmp[r] += dm[r];
+        } else {
+            const float* crow = child + i * R;
+            double U[n_chol(NMAX)];
+            for (int r = 0; r < n; ++r)
+                for (int c = 0; c <= r; ++c) {
+                    const double raw = (double)crow[n + tri(r, c)];
+                    U[tri(r, c)] = (r == c) ? exp(raw) : act_offdiag(raw);
+                }
+            for (int r = 0; r < n; ++r)
+                for (int c = 0; c <= r; ++c) {
+                    double s1 = 0.0, s2 = 0.0;
+                    for (int k = 0; k <= c; ++k) s1 += GL[r * n + k] * U[tri(c, k)];   // (G U^T)_rc
+                    for (int k = r; k < n; ++k) s2 += Lp[tri(k, r)] * GL[k * n + c];  // (L^T G)_rc
+                    GLp[r * n + c] += s1 + dm[r] * (double)crow[c];
+                    const double d = s2 * (r == c ? U[tri(r, r)] : (1.0 - U[tri(r, c)] * U[tri(r, c)]) * 0.5);
+                    out[n + tri(r, c)] = (float)d;
+                }
+            for (int r = 0; r < n; ++r) {
+                double s = 0.0;
+                for (int k = r; k < n; ++k) s += Lp[tri(k, r)] * dm[k];
+                out[r] = (float)s;
+                dmp[r] += dm[r];
+            }
+        }
+    }
+    for (int r = 0; r < n; ++r) op[r] = (float)dmp[r];
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c <= r; ++c) {
+            const double l = Lp[tri(r, c)];
+            op[n + tri(r, c)] = (float)(GLp[r * n + c] * (r == c ? l : (1.0 - l * l) * 0.5));
+        }
+    // non-finite gradient -> NonFiniteGradientError
+    for (int which = 0; which < nev; ++which) {
+        const float* out = which ? oc : op;
+        for (int t = 0; t < R; ++t)
+            if (!isfinite(out[t])) {
+                record_key(&st->nonfinite_key, (which ? G * R : 0) + i * R + t);
+                break;
+            }
+    }
+}
+
+extern "C" int ndg_epilogue(int n, int64_t G, int64_t Gev, int amp_mode, const float* params, const float* child,
+                            const uint8_t* flags, const uint8_t* eflags, const double* chol64, const double* accum,
+                            float* grad_params, float* grad_child, float* stats, ndg_status* status, void* stream) {
+    if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
+    NDG_REQUIRE(Gev == G || Gev == 2 * G, "Gev must be G or 2G");
+    NDG_REQUIRE(Gev == G || (child && grad_child), "child rows and child gradients required when Gev == 2G");
+    if (G == 0) return NDG_OK;
+    int threads = 64;
+    epilogue_kernel<<<(unsigned)((G + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+        n, G, Gev, amp_mode, params, child, flags, eflags, chol64, accum, grad_params,
+        Gev == 2 * G ? grad_child : nullptr, stats, status);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K9 Adam with per-block learning rates.
+// ---------------------------------------------------------------------------------------------
+__global__ void adam_kernel(int n, int64_t rows, float* __restrict__ p, const float* __restrict__ g,
+                            float* __restrict__ m1, float* __restrict__ m2, const uint8_t* __restrict__ row_mask,
+                            float c1, float c2, float lr_mean, float lr_chol, float lr_color, float lr_amp, float b1,
+                            float b2, float eps) {
+    const int R = raw_floats(n), P = n_chol(n);
+    const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (x >= rows * R) return;
+    const int64_t row = x / R;
+    const int col = (int)(x - row * R);
+    if (row_mask && !row_mask[row]) return;
+    const float lr = col < n ? lr_mean : (col < n + P ? lr_chol : (col < n + P + 3 ? lr_color : lr_amp));
+    const float gv = g[x];
+    const float a = __fadd_rn(__fmul_rn(b1, m1[x]), __fmul_rn(1.f - b1, gv));
+    const float b = __fadd_rn(__fmul_rn(b2, m2[x]), __fmul_rn(__fmul_rn(1.f - b2, gv), gv));
+    m1[x] = a;
+    m2[x] = b;
+    p[x] = __fsub_rn(p[x], __fdiv_rn(__fmul_rn(lr, __fdiv_rn(a, c1)), __fadd_rn(__fsqrt_rn(__fdiv_rn(b, c2)), eps)));
+}
+
+extern "C" int ndg_adam(int n, int64_t rows, float* params, const float* grad, float* m1, float* m2,
+                        const uint8_t* row_mask, int step, float lr_mean, float lr_chol, float lr_color, float lr_amp,
+                        float beta1, float beta2, float eps, void* stream) {
+    if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
+    NDG_REQUIRE(step >= 1, "adam step counter starts at 1");
+    const int64_t total = rows * raw_floats(n);
+    if (total == 0) return NDG_OK;
+    const float c1 = (float)(1.0 - pow((double)beta1, step));
+    const float c2 = (float)(1.0 - pow((double)beta2, step));
+    int threads = 256;
+    adam_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+        n, rows, params, grad, m1, m2, row_mask, c1, c2, lr_mean, lr_chol, lr_color, lr_amp, beta1, beta2, eps);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}

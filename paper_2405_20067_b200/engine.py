@@ -1,0 +1,357 @@
+"""The culled forward + backward hot path on one GPU, one C-ABI call per stage.
+
+Host side of the reference's L1-L3 hot path: the operations of SPEC.md's
+gmm-core, culling and grad modules, each enqueued on the current CUDA stream through libndg.so:
+
+    K1 ndg_prologue      activate_cholesky + compose_child + activations
+    K2 ndg_project       project_components
+    K3 ndg_tile_bounds   TileBounds
+    K4 ndg_cull_*        cull_tile for every tile -> CSR candidate lists
+    K5 ndg_forward       eval_mixture (+ K6 loss_rel_l2 fused)
+    K7 ndg_backward      backward pair loop
+    K8 ndg_epilogue      backward tail, raw-parameter chain rule
+    K9 ndg_adam          adam_step
+
+There is no CPU path: everything below requires libndg.so and a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .errors import InvalidParameterError, NonFiniteGradientError
+from .gmm import Mixture, n_chol, raw_width
+
+_INT64_MAX = (1 << 63) - 1
+_BLOCKS = ("mean", "chol", "color", "amp")
+
+
+def _p(t):
+    """Device pointer of a tensor (0 for None)."""
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+# ----------------------------------------------------------------------------------------------
+# culling types
+# ----------------------------------------------------------------------------------------------
+@dataclass
+class ProjectionSet:
+    """k unit vectors in R^N reproducible from seed."""
+    vectors: np.ndarray            # [k, N] float64
+    seed: int
+    device_vectors: torch.Tensor = field(default=None, repr=False)
+
+    @property
+    def k(self):
+        return self.vectors.shape[0]
+
+    def on(self, device):
+        if self.device_vectors is None or self.device_vectors.device != device:
+            self.device_vectors = torch.from_numpy(np.ascontiguousarray(self.vectors)).to(device)
+        return self.device_vectors
+
+
+def make_projection_set(n_dims: int, k: int = 16, seed: int = 0) -> ProjectionSet:
+    """normalised independent standard normals. The stream is pinned to
+    numpy.random.default_rng(seed).standard_normal((k, N)) and the norm to a sequential float64 sum
+    of squares."""
+    if n_dims < 1 or k < 1:
+        raise ValueError("n_dims and k must be >= 1")
+    v = np.random.default_rng(seed).standard_normal((k, n_dims))
+    ss = v[:, 0] * v[:, 0]
+    for j in range(1, n_dims):
+        ss = ss + v[:, j] * v[:, j]
+    return ProjectionSet(v / np.sqrt(ss)[:, None], int(seed))
+
+
+@dataclass
+class EvalRecords:
+    """Output of K1 for the evaluated Gaussians (index space e = i | G + i)."""
+    Gev: int
+    rec: torch.Tensor        # [Gev, RS] float32 evaluation records
+    mean64: torch.Tensor     # [Gev, N] float64
+    chol64: torch.Tensor     # [Gev, P] float64 packed lower factor (composed for children)
+    eflags: torch.Tensor     # [Gev] uint8: bit0 live, bit1 degenerate
+
+
+@dataclass
+class ProjectedBounds:
+    """SPEC.md:161-167, laid out [k, Gev]; thr = multiplier * sigma_r, -1 when never evaluated."""
+    m_r: torch.Tensor
+    sigma_r: torch.Tensor
+    thr: torch.Tensor
+    multiplier: float
+
+
+@dataclass
+class TileBounds:
+    """lo / hi [T, k]."""
+    lo: torch.Tensor
+    hi: torch.Tensor
+    tile_size: int
+
+
+@dataclass
+class CandidateLists:
+    """Per-tile active sets as CSR (offsets int64 [T+1], idx int32 ascending per tile)."""
+    offsets: torch.Tensor
+    idx: torch.Tensor
+    chunk_offsets: torch.Tensor
+    n_pairs_tiles: int        # sum over tiles of |cand(tile)|
+    n_chunks: int
+
+    @property
+    def T(self):
+        return int(self.offsets.shape[0]) - 1
+
+    def kept_fraction(self, Gev: int) -> float:
+        return self.n_pairs_tiles / max(1, self.T * Gev)
+
+
+@dataclass
+class GradientBuffer:
+    """Raw-layout gradients of parents and children plus the density-control
+    statistics, all views into ONE flat float32 buffer so a multi-GPU step needs one allreduce."""
+    flat: torch.Tensor
+    params: torch.Tensor      # [G, R]
+    child: torch.Tensor       # [G, R]
+    stats: torch.Tensor       # [Gev, 3]: loss share, gradient proxy, pairs
+    scalars: torch.Tensor     # [2]: loss, total pairs (filled by the caller that reduces)
+
+
+@dataclass
+class StepResult:
+    loss: float
+    pred: torch.Tensor
+    grads: GradientBuffer
+    candidates: CandidateLists
+    n_degenerate: int
+    kept_fraction: float
+
+
+def alloc_gradients(G: int, Gev: int, n: int, device) -> GradientBuffer:
+    R = raw_width(n)
+    flat = torch.zeros(2 * G * R + 3 * Gev + 2, dtype=torch.float32, device=device)
+    o = 0
+    gp = flat[o:o + G * R].view(G, R); o += G * R
+    gc = flat[o:o + G * R].view(G, R); o += G * R
+    st = flat[o:o + 3 * Gev].view(Gev, 3); o += 3 * Gev
+    return GradientBuffer(flat, gp, gc, st, flat[o:o + 2])
+
+
+class HotPath:
+    """One object per (device, N). Each method is one stage; `fwd_bwd` chains them."""
+
+    def __init__(self, n_dims: int, *, k: int = 16, multiplier: float = 3.0, tile_size: int = 256,
+                 eps: float = 0.01, projection_seed: int = 0, projections: ProjectionSet | None = None,
+                 device=None):
+        self.n = int(n_dims)
+        self.L = K.layout(self.n)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if self.device.type != "cuda":
+            raise RuntimeError("HotPath needs a CUDA device (no CPU fallback)")
+        self.ps = projections or make_projection_set(self.n, k, projection_seed)
+        self.multiplier = float(multiplier)
+        self.tile = int(tile_size)
+        self.eps = float(eps)
+        self.status = torch.zeros(4, dtype=torch.int64, device=self.device)
+
+    # -- K1 --------------------------------------------------------------------------------
+    def activate(self, mix: Mixture) -> EvalRecords:
+        n, G, Gev = self.n, mix.G, mix.Gev
+        dev = self.device
+        rec = torch.empty(Gev, self.L["rec"], dtype=torch.float32, device=dev)
+        mean64 = torch.empty(Gev, n, dtype=torch.float64, device=dev)
+        chol64 = torch.empty(Gev, n_chol(n), dtype=torch.float64, device=dev)
+        eflags = torch.empty(Gev, dtype=torch.uint8, device=dev)
+        K.call("ndg_prologue", n, G, Gev, mix.amp_mode, _p(mix.params), _p(mix.child), _p(mix.flags), _p(rec),
+               _p(mean64), _p(chol64), _p(eflags), _p(self.status), _stream())
+        return EvalRecords(Gev, rec, mean64, chol64, eflags)
+
+    # -- K2 --------------------------------------------------------------------------------
+    def project(self, recs: EvalRecords) -> ProjectedBounds:
+        k, Gev = self.ps.k, recs.Gev
+        m_r = torch.empty(k, Gev, dtype=torch.float64, device=self.device)
+        s_r = torch.empty_like(m_r)
+        thr = torch.empty_like(m_r)
+        K.call("ndg_project", self.n, Gev, _p(recs.mean64), _p(recs.chol64), _p(recs.eflags),
+               _p(self.ps.on(self.device)), k, self.multiplier, _p(m_r), _p(s_r), _p(thr), _stream())
+        return ProjectedBounds(m_r, s_r, thr, self.multiplier)
+
+    # -- K3 --------------------------------------------------------------------------------
+    def tile_bounds(self, queries: torch.Tensor) -> TileBounds:
+        B = int(queries.shape[0])
+        if B % self.tile:
+            raise ValueError("batch size must be a multiple of tile_size (SPEC.md:441-442)")
+        T, k = B // self.tile, self.ps.k
+        lo = torch.empty(T, k, dtype=torch.float64, device=self.device)
+        hi = torch.empty_like(lo)
+        K.call("ndg_tile_bounds", self.n, B, self.tile, _p(queries), _p(self.ps.on(self.device)), k, _p(lo), _p(hi),
+               _stream())
+        return TileBounds(lo, hi, self.tile)
+
+    # -- K4 --------------------------------------------------------------------------------
+    def cull(self, tb: TileBounds, pb: ProjectedBounds) -> CandidateLists:
+        T, k = int(tb.lo.shape[0]), int(tb.lo.shape[1])
+        Gev = int(pb.m_r.shape[1])
+        W = (Gev + 31) // 32
+        mask = torch.empty(T, W, dtype=torch.int32, device=self.device)
+        counts = torch.zeros(T, dtype=torch.int64, device=self.device)
+        K.call("ndg_cull_mask", T, k, Gev, _p(tb.lo), _p(tb.hi), _p(pb.m_r), _p(pb.thr), _p(mask), _p(counts),
+               _stream())
+        return self._finish_lists(T, Gev, counts, mask)
+
+    def all_active(self, T: int, recs: EvalRecords) -> CandidateLists:
+        """Culling disabled (SPEC.md:276 finite differences, SPEC.md:562 --no-cull): every live
+        Gaussian is a candidate of every tile (still via the device compaction kernel)."""
+        Gev = recs.Gev
+        W = (Gev + 31) // 32
+        live = (recs.eflags & 1).to(torch.bool)
+        pad = torch.zeros(W * 32, dtype=torch.bool, device=self.device)
+        pad[:Gev] = live
+        bits = pad.view(W, 32).to(torch.int64) << torch.arange(32, device=self.device, dtype=torch.int64)
+        words = bits.sum(dim=1).to(torch.int64)
+        words = torch.where(words >= 2 ** 31, words - 2 ** 32, words).to(torch.int32)
+        mask = words.unsqueeze(0).expand(T, W).contiguous()
+        counts = live.sum().to(torch.int64).repeat(T)
+        return self._finish_lists(T, Gev, counts, mask)
+
+    def _finish_lists(self, T, Gev, counts, mask) -> CandidateLists:
+        offsets = torch.empty(T + 1, dtype=torch.int64, device=self.device)
+        chunk_off = torch.empty(T + 1, dtype=torch.int64, device=self.device)
+        K.call("ndg_scan_counts", T, _p(counts), _p(offsets), _p(chunk_off), _stream())
+        tot = torch.stack([offsets[T], chunk_off[T]]).cpu()   # the step's one mid-pipeline sync: sizes idx
+        nnz, nchunks = int(tot[0]), int(tot[1])
+        idx = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.device)
+        K.call("ndg_cull_compact", T, Gev, _p(mask), _p(offsets), _p(idx), _stream())
+        return CandidateLists(offsets, idx[:nnz], chunk_off, nnz, nchunks)
+
+    # -- K5 + K6 ---------------------------------------------------------------------------
+    def forward(self, queries, recs: EvalRecords, cl: CandidateLists, targets=None, n_total=None):
+        B = int(queries.shape[0])
+        T = B // self.tile
+        pred = torch.empty(B, 3, dtype=torch.float32, device=self.device)
+        qrec = loss_part = None
+        if targets is not None:
+            qrec = torch.empty(B, self.L["qrec"], dtype=torch.float32, device=self.device)
+            loss_part = torch.empty(T, dtype=torch.float64, device=self.device)
+        K.call("ndg_forward", self.n, B, self.tile, _p(queries), _p(targets), _p(recs.rec), _p(cl.offsets), _p(cl.idx),
+               self.eps, int(n_total or B), _p(pred), _p(qrec), _p(loss_part), _stream())
+        return pred, qrec, loss_part
+
+    def finalize_loss(self, loss_part) -> torch.Tensor:
+        out = torch.empty(1, dtype=torch.float64, device=self.device)
+        K.call("ndg_loss_finalize", int(loss_part.shape[0]), _p(loss_part), _p(out), _stream())
+        return out
+
+    # -- K7 + K8 ---------------------------------------------------------------------------
+    def backward(self, mix: Mixture, recs: EvalRecords, cl: CandidateLists, qrec, grads: GradientBuffer):
+        B = int(qrec.shape[0])
+        accum = torch.zeros(recs.Gev, self.L["acc"], dtype=torch.float64, device=self.device)
+        K.call("ndg_backward", self.n, B, self.tile, _p(qrec), _p(recs.rec), _p(cl.offsets), _p(cl.idx),
+               _p(cl.chunk_offsets), cl.n_chunks, _p(accum), _stream())
+        K.call("ndg_epilogue", self.n, mix.G, recs.Gev, mix.amp_mode, _p(mix.params), _p(mix.child), _p(mix.flags),
+               _p(recs.eflags), _p(recs.chol64), _p(accum), _p(grads.params), _p(grads.child), _p(grads.stats),
+               _p(self.status), _stream())
+        return accum
+
+    # -- status ----------------------------------------------------------------------------
+    def reset_status(self):
+        self.status.zero_()
+
+    def check_status(self, mix: Mixture, host_status=None):
+        st = (self.status.cpu() if host_status is None else host_status).tolist()
+        R = raw_width(self.n)
+        for slot, cls in ((0, InvalidParameterError), (1, NonFiniteGradientError)):
+            if st[slot] != 0:
+                key = _INT64_MAX - st[slot]
+                which = "child" if key >= mix.G * R else "parent"
+                key %= mix.G * R
+                comp, entry = divmod(key, R)
+                n = self.n
+                blk = 0 if entry < n else 1 if entry < n + n_chol(n) else 2 if entry < n + n_chol(n) + 3 else 3
+                if cls is InvalidParameterError:
+                    raise InvalidParameterError(f"non-finite raw parameter ({which} row, block {_BLOCKS[blk]})",
+                                                component=int(comp), block=_BLOCKS[blk], entry=int(entry))
+                raise NonFiniteGradientError(f"non-finite gradient ({which} row, block {_BLOCKS[blk]})",
+                                             component=int(comp), block=_BLOCKS[blk], batch_index=-1)
+        return int(st[2])
+
+    # -- whole step ------------------------------------------------------------------------
+    def fwd_bwd(self, mix: Mixture, queries, targets, *, cull: bool = True, n_total=None, grads=None,
+                allreduce=None, check: bool = True) -> StepResult:
+        """One culled forward + loss + backward pass (SPEC.md:329 minus the optimizer step).
+
+        `allreduce(flat)` -- when given -- sums the flat gradient buffer across ranks (one NCCL
+        collective) before the status / loss read-back."""
+        self.reset_status()
+        recs = self.activate(mix)
+        T = int(queries.shape[0]) // self.tile
+        if cull:
+            pb = self.project(recs)
+            tb = self.tile_bounds(queries)
+            cl = self.cull(tb, pb)
+        else:
+            cl = self.all_active(T, recs)
+        pred, qrec, loss_part = self.forward(queries, recs, cl, targets, n_total)
+        loss = self.finalize_loss(loss_part)
+        if grads is None:
+            grads = alloc_gradients(mix.G, recs.Gev, self.n, self.device)
+        self.backward(mix, recs, cl, qrec, grads)
+        grads.scalars[0] = loss[0].to(torch.float32)
+        grads.scalars[1] = float(cl.n_pairs_tiles * self.tile)
+        if allreduce is not None:
+            allreduce(grads.flat)
+        host = torch.cat([self.status, loss.view(torch.int64)]).cpu()
+        n_deg = self.check_status(mix, host[:4]) if check else 0
+        loss_v = float(host[4:5].view(torch.float64)[0]) if allreduce is None else float(grads.scalars[0])
+        return StepResult(loss_v, pred, grads, cl, n_deg, cl.kept_fraction(recs.Gev))
+
+    def evaluate(self, mix: Mixture, queries, *, cull: bool = True) -> torch.Tensor:
+        """Culled evaluation at every query (cmd_eval's path)."""
+        self.reset_status()
+        recs = self.activate(mix)
+        T = int(queries.shape[0]) // self.tile
+        cl = self.cull(self.tile_bounds(queries), self.project(recs)) if cull else self.all_active(T, recs)
+        pred, _, _ = self.forward(queries, recs, cl)
+        self.check_status(mix)
+        return pred
+
+
+def adam_step(mix: Mixture, grads: GradientBuffer, state, step: int, lr=(2e-3, 5e-3, 1e-2, 1e-2),
+              betas=(0.9, 0.999), eps=1e-8):
+    """K9: bias-corrected Adam with per-block learning rates, applied to
+    parent rows (not frozen) and live child rows. `state` = dict(m1p, m2p, m1c, m2c) float32."""
+    n = mix.n_dims
+    fr = (mix.flags & 2) == 0
+    pmask = fr.to(torch.uint8).contiguous()
+    K.call("ndg_adam", n, mix.G, _p(mix.params), _p(grads.params), _p(state["m1p"]), _p(state["m2p"]), _p(pmask),
+           int(step), *[float(x) for x in lr], float(betas[0]), float(betas[1]), float(eps), _stream())
+    if mix.children_live:
+        cmask = (((mix.flags & 1) != 0) & fr).to(torch.uint8).contiguous()
+        K.call("ndg_adam", n, mix.G, _p(mix.child), _p(grads.child), _p(state["m1c"]), _p(state["m2c"]), _p(cmask),
+               int(step), *[float(x) for x in lr], float(betas[0]), float(betas[1]), float(eps), _stream())
+
+
+def new_adam_state(mix: Mixture):
+    z = lambda: torch.zeros_like(mix.params)  # noqa: E731
+    return dict(m1p=z(), m2p=z(), m1c=z(), m2c=z())
+
+
+def kept_pairs_flops(n: int) -> int:
+    """Canonical algorithmic FP32 flops per (query, candidate) pair for fwd+bwd:
+    F(N) = 3N^2 + 9N + 22 (184 / 412 / 934 at N = 6 / 10 / 16)."""
+    return 3 * n * n + 9 * n + 22
+
+
+def math_isfinite(x: float) -> bool:
+    return math.isfinite(x)

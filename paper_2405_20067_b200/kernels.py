@@ -1,0 +1,93 @@
+"""ctypes binding of libndg.so -- the slot the reference fills with ``ndgauss.kernels._core``
+(/root/reference/pkg/setup.py:32-53).
+
+Unlike the reference (which silently falls back to NumPy when the extension is missing,
+pkg/setup.py:3-4, 14-29), there is exactly one backend: if libndg.so is absent or no CUDA device is
+visible, every hot-path call raises. Every entry point is declared in include/ndg.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libndg.so")
+
+_P = C.c_void_p
+_I = C.c_int
+_L = C.c_int64
+_F = C.c_float
+_D = C.c_double
+
+# name -> argtypes, mirroring include/ndg.h one-to-one (tests/test_abi.py checks the export list)
+SIGNATURES = {
+    "ndg_abi_version": [],
+    "ndg_last_error": [],
+    "ndg_supported_dims": [_I],
+    "ndg_raw_floats": [_I],
+    "ndg_record_floats": [_I],
+    "ndg_query_floats": [_I],
+    "ndg_accum_doubles": [_I],
+    "ndg_num_stats": [],
+    "ndg_backward_chunk": [],
+    "ndg_prologue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "ndg_project": [_I, _L, _P, _P, _P, _P, _I, _D, _P, _P, _P, _P],
+    "ndg_tile_bounds": [_I, _L, _I, _P, _P, _I, _P, _P, _P],
+    "ndg_cull_mask": [_L, _I, _L, _P, _P, _P, _P, _P, _P, _P],
+    "ndg_scan_counts": [_L, _P, _P, _P, _P],
+    "ndg_cull_compact": [_L, _L, _P, _P, _P, _P],
+    "ndg_forward": [_I, _L, _I, _P, _P, _P, _P, _P, _F, _L, _P, _P, _P, _P],
+    "ndg_loss_finalize": [_L, _P, _P, _P],
+    "ndg_backward": [_I, _L, _I, _P, _P, _P, _P, _P, _L, _P, _P],
+    "ndg_epilogue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "ndg_adam": [_I, _L, _P, _P, _P, _P, _P, _I, _F, _F, _F, _F, _F, _F, _F, _P],
+}
+
+ERRORS = {0: "NDG_OK", 1: "NDG_ERR_INVALID_PARAMETER", 2: "NDG_ERR_NONFINITE_GRADIENT",
+          -1: "NDG_ERR_BAD_ARGUMENT", -2: "NDG_ERR_UNSUPPORTED_DIMS", -3: "NDG_ERR_CUDA"}
+
+_lib = None
+
+
+class KernelLibraryMissing(RuntimeError):
+    pass
+
+
+def load():
+    """Load libndg.so (no CUDA call is made; safe on a CPU-only host)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise KernelLibraryMissing(
+            f"{LIB_PATH} is not built -- run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = C.c_char_p if name == "ndg_last_error" else C.c_int
+    _lib = lib
+    return lib
+
+
+class NdgLaunchError(RuntimeError):
+    pass
+
+
+def call(name: str, *args):
+    """Invoke an entry point; a nonzero launch code raises with the library's error string."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.ndg_last_error().decode(errors="replace")
+        raise NdgLaunchError(f"{name} failed: {ERRORS.get(rc, rc)} {msg}")
+    return rc
+
+
+def layout(n: int) -> dict:
+    lib = load()
+    if not lib.ndg_supported_dims(n):
+        raise ValueError(f"n_dims={n} not supported (1..16)")
+    return dict(raw=lib.ndg_raw_floats(n), rec=lib.ndg_record_floats(n), qrec=lib.ndg_query_floats(n),
+                acc=lib.ndg_accum_doubles(n), stats=lib.ndg_num_stats(), chunk=lib.ndg_backward_chunk())

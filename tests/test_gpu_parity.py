@@ -1,0 +1,202 @@
+"""GPU parity: every stage of the CUDA hot path (through the C ABI) against the CPU oracle.
+
+Bars:
+  * candidate lists (CSR offsets + indices), tile bounds and projected means: bit-exact;
+  * sigma_r given the same activated factors: bit-exact; activated factors vs oracle: 1e-15 rel;
+  * pred, loss, gradients: block-relative ||gpu - ref|| <= RTOL * ||ref|| with RTOL = 1e-4
+    (north_star's FP32 tolerance), per block (mean / chol / color / amp, parent / child).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ndg_oracle as O
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-4
+
+
+def _ndg():
+    import paper_2405_20067_b200 as ndg
+    return ndg
+
+
+def _mk(N, G, B, *, children=False, amp_mode=0, seed=0, regime="R", sigma0=None):
+    ndg = _ndg()
+    om, _ = O.synthetic_mixture(N, G, seed=seed, children=children, amp_mode=amp_mode, sigma0=sigma0)
+    q = O.synthetic_queries(N, B, seed=seed + 1, regime=regime)
+    t = O.synthetic_targets(B, seed=seed + 3)
+    mix = ndg.Mixture.from_arrays(N, amp_mode, om.params, om.child, om.has_child, om.frozen)
+    return om, mix, q, t
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _check_grads(N, got, ref, tag):
+    ms, cs, cols, amp = O.raw_slices(N)
+    for name, sl in (("mean", ms), ("chol", cs), ("color", cols), ("amp", slice(amp, amp + 1))):
+        r = ref[:, sl]
+        if np.linalg.norm(r) == 0:
+            assert np.linalg.norm(got[:, sl]) <= 1e-12, (tag, name)
+            continue
+        e = _rel(got[:, sl], r)
+        assert e < RTOL, f"{tag}.{name}: block-relative error {e:.3e} >= {RTOL}"
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 6, 10, 16])
+@pytest.mark.parametrize("amp_mode", [0, 1])
+def test_prologue_activation(cuda, N, amp_mode):
+    ndg = _ndg()
+    om, mix, q, t = _mk(N, 300, 256, children=True, amp_mode=amp_mode)
+    hp = ndg.HotPath(N)
+    recs = hp.activate(mix)
+    ev = O.build_eval_set(om)
+    P = O.n_chol(N)
+    Lref = np.stack([ev.L[:, i, j] for i in range(N) for j in range(i + 1)], axis=1)
+    assert np.allclose(recs.mean64.cpu().numpy(), ev.mean, rtol=1e-14, atol=1e-15)
+    assert np.allclose(recs.chol64.cpu().numpy(), Lref, rtol=1e-14, atol=1e-15)
+    ef = recs.eflags.cpu().numpy()
+    assert np.array_equal(ef & 1, ev.live.astype(np.uint8))
+    assert P == recs.chol64.shape[1]
+
+
+@pytest.mark.parametrize("N", [2, 6, 10, 16])
+def test_projection_tilebounds_cull_bitexact(cuda, N):
+    ndg = _ndg()
+    om, mix, q, t = _mk(N, 700, 2048, children=True, regime="C" if N > 6 else "R")
+    hp = ndg.HotPath(N, projection_seed=5)
+    recs = hp.activate(mix)
+    pb = hp.project(recs)
+    qd = torch.from_numpy(q).cuda()
+    tb = hp.tile_bounds(qd)
+    cl = hp.cull(tb, pb)
+    torch.cuda.synchronize()
+    # oracle on the GPU's own activated factors -> every float64 quantity must match bit for bit
+    ev = O.build_eval_set(om)
+    Lg = np.zeros_like(ev.L)
+    c64 = recs.chol64.cpu().numpy()
+    for i in range(N):
+        for j in range(i + 1):
+            Lg[:, i, j] = c64[:, O.tri(i, j)]
+    ev.L = Lg
+    ev.mean = recs.mean64.cpu().numpy()
+    mr, sr, thr = O.project_components(ev, hp.ps.vectors, 3.0)
+    assert np.array_equal(pb.m_r.cpu().numpy(), mr)
+    assert np.array_equal(pb.sigma_r.cpu().numpy(), sr)
+    assert np.array_equal(pb.thr.cpu().numpy(), thr)
+    lo, hi = O.tile_bounds(q, hp.ps.vectors, 256)
+    assert np.array_equal(tb.lo.cpu().numpy(), lo) and np.array_equal(tb.hi.cpu().numpy(), hi)
+    off, idx = O.cull_csr(lo, hi, mr, thr)
+    assert np.array_equal(cl.offsets.cpu().numpy(), off)
+    assert np.array_equal(cl.idx.cpu().numpy(), idx)
+    # and end to end against the fully independent oracle (activations computed on the CPU)
+    ev2 = O.build_eval_set(om)
+    mr2, sr2, thr2 = O.project_components(ev2, hp.ps.vectors, 3.0)
+    off2, idx2 = O.cull_csr(lo, hi, mr2, thr2)
+    assert np.array_equal(cl.offsets.cpu().numpy(), off2) and np.array_equal(cl.idx.cpu().numpy(), idx2)
+
+
+@pytest.mark.parametrize("N,G,B,children,amp_mode,regime", [
+    (1, 50, 512, False, 0, "R"),
+    (2, 200, 1024, True, 1, "R"),
+    (4, 300, 1024, True, 0, "C"),
+    (6, 512, 2048, True, 0, "R"),
+    (8, 300, 1024, False, 1, "R"),
+    (10, 400, 1024, True, 0, "R"),
+    (10, 600, 2048, False, 1, "C"),
+    (16, 200, 512, True, 0, "R"),
+])
+def test_fwd_bwd_parity(cuda, N, G, B, children, amp_mode, regime):
+    ndg = _ndg()
+    om, mix, q, t = _mk(N, G, B, children=children, amp_mode=amp_mode, regime=regime)
+    hp = ndg.HotPath(N, projection_seed=2)
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
+    assert np.array_equal(res.candidates.offsets.cpu().numpy(), ref["offsets"])
+    assert np.array_equal(res.candidates.idx.cpu().numpy(), ref["idx"])
+    assert _rel(res.pred.cpu().numpy(), ref["pred"]) < RTOL
+    assert abs(res.loss - ref["loss"]) <= RTOL * abs(ref["loss"])
+    _check_grads(N, res.grads.params.cpu().numpy(), ref["grad_parent"], "parent")
+    if children:
+        _check_grads(N, res.grads.child.cpu().numpy(), ref["grad_child"], "child")
+    st = res.grads.stats.cpu().numpy()
+    for j in range(3):
+        assert _rel(st[:, j], ref["stats"][:, j]) < RTOL, f"stat {j}"
+
+
+def test_cfg1_full_size_vs_c_oracle(cuda):
+    """BASELINE.json configs[0] at full size: 6-D, 4096 Gaussians, 16384 queries (64 tiles)."""
+    from oracle import c_oracle as CO
+    ndg = _ndg()
+    om, mix, q, t = _mk(6, 4096, 16384, seed=0)
+    hp = ndg.HotPath(6, projection_seed=2)
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    ref = CO.step(om, q, t, hp.ps.vectors)
+    assert np.array_equal(res.candidates.offsets.cpu().numpy(), ref["offsets"])
+    assert np.array_equal(res.candidates.idx.cpu().numpy(), ref["idx"])
+    assert _rel(res.pred.cpu().numpy(), ref["pred"]) < RTOL
+    assert abs(res.loss - ref["loss"]) <= RTOL * abs(ref["loss"])
+    _check_grads(6, res.grads.params.cpu().numpy(), ref["grad_parent"], "parent")
+
+
+def test_culled_get_zero_gradient_and_cull_on_off(cuda):
+    """SPEC.md:285 (culled -> exactly zero gradient) and SPEC.md:528 (cull on vs off < 1e-6)."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(6, 2000, 2048, regime="C")
+    hp = ndg.HotPath(6, projection_seed=2)
+    qd, td = torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda()
+    res = hp.fwd_bwd(mix, qd, td)
+    used = np.zeros(mix.G, bool)
+    used[np.unique(res.candidates.idx.cpu().numpy())] = True
+    assert (~used).sum() > 0
+    assert np.all(res.grads.params.cpu().numpy()[~used] == 0.0)
+    on = hp.evaluate(mix, qd, cull=True).cpu().numpy()
+    off = hp.evaluate(mix, qd, cull=False).cpu().numpy()
+    # conservativeness consequence: every culled pair has g <= exp(-mult^2/2), so per query
+    # |on - off| <= exp(-4.5) * sum over that tile's culled Gaussians of a
+    ev = O.build_eval_set(om)
+    off_r = O.forward(q, ev, *O.all_active_csr(q.shape[0] // 256, ev))
+    assert _rel(off, off_r) < RTOL
+    counts = np.diff(res.candidates.offsets.cpu().numpy())
+    idx = res.candidates.idx.cpu().numpy()
+    for tt in range(q.shape[0] // 256):
+        culled = np.setdiff1d(np.arange(mix.G), idx[res.candidates.offsets[tt].item():][:counts[tt]])
+        bound = np.exp(-4.5) * ev.a[culled].sum(axis=0) + 1e-6
+        assert np.all(np.abs(on - off)[tt * 256:(tt + 1) * 256] <= bound)
+    # at a 6-sigma multiplier the culled tail is below 1e-6 per channel (SPEC.md:528's property)
+    hp6 = ndg.HotPath(6, projection_seed=2, multiplier=6.0)
+    on6 = hp6.evaluate(mix, qd, cull=True).cpu().numpy()
+    assert np.max(np.abs(on6 - off)) < 1e-6
+
+
+def test_invalid_parameter_reported(cuda):
+    ndg = _ndg()
+    om, mix, q, t = _mk(4, 64, 256)
+    p = mix.params.clone()
+    p[17, 5] = float("nan")
+    p[40, 2] = float("inf")
+    mix.params = p
+    hp = ndg.HotPath(4)
+    with pytest.raises(ndg.InvalidParameterError) as ei:
+        hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    assert ei.value.component == 17 and ei.value.entry == 5 and ei.value.block == "chol"
+
+
+def test_adam_matches_oracle(cuda):
+    ndg = _ndg()
+    om, mix, q, t = _mk(5, 100, 256)
+    rng = np.random.default_rng(0)
+    g = rng.normal(size=mix.params.shape).astype(np.float32)
+    grads = ndg.alloc_gradients(mix.G, mix.G, 5, mix.device)
+    grads.params.copy_(torch.from_numpy(g))
+    state = ndg.new_adam_state(mix)
+    p0 = mix.params.cpu().numpy()
+    ndg.adam_step(mix, grads, state, step=1)
+    ndg.adam_step(mix, grads, state, step=2)
+    lr = O.block_lr(5)
+    p, m1, m2 = O.adam_step(p0, g, np.zeros_like(p0), np.zeros_like(p0), 1, lr)
+    p, m1, m2 = O.adam_step(p, g, m1, m2, 2, lr)
+    assert np.array_equal(mix.params.cpu().numpy(), p)
