@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the culled N-D Gaussian-mixture fwd+bwd step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--regime R|C]
+
+Workload (BASELINE.json configs[1], the metric's configuration): 10-D mixture of 100k Gaussians,
+2^20 queries per GPU per step, tiles of 256 queries sorted by dim 0 (regime R, the reference
+sampler SPEC.md:443), k = 16 projection vectors, multiplier 3, relative-L2 loss eps 0.01.
+A step = K1 prologue, K2 projections, K3 tile bounds, K4 binning, K5+K6 forward+loss,
+K7 backward, K8 epilogue, [NCCL allreduce of the flat gradient buffer when N > 1], K9 Adam.
+`value` = queries processed by all ranks / max-over-ranks device time of K steps (CUDA events),
+inputs resident in HBM, L2 flushed (256 MiB write) before every timed step.
+`e2e` = the same step through the public API with pinned-host inputs copied in every step and the
+loss read back. Rank 0 prints one JSON line.
+
+--impl reference times the reference's CPU path on the host cores: the reference ships no
+runnable implementation, so this is oracle/ndg_oracle.c -- the C/OpenMP
+restatement of SPEC.md standing in for the reference's intended `_core` (pkg/setup.py:36-43) --
+on a bounded sample of the same workload, extrapolated per tile to the full batch.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "culled query evals/sec (fwd+bwd) at 10-D, 1/2/4/8 B200; % of FP32/HBM roofline"
+NOMINAL_FP32_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12     # 74.4, datasheet-class (not measured)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--regime", choices=["R", "C"], default="R")
+    ap.add_argument("--n-dims", type=int, default=10)
+    ap.add_argument("--gaussians", type=int, default=100_000)
+    ap.add_argument("--batch", type=int, default=1 << 20, help="queries per GPU per step")
+    ap.add_argument("--tile", type=int, default=256)
+    ap.add_argument("--k", type=int, default=16)
+    ap.add_argument("--children", action="store_true", help="every component carries a live child (Gev = 2G)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the regime-C secondary measurement")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample duration")
+    return ap.parse_args()
+
+
+def workload_name(a, regime):
+    return (f"cfg2: {a.n_dims}-D synthetic shading-shaped mixture, {a.gaussians} Gaussians"
+            f"{' (+live children)' if a.children else ''}, {a.batch} queries/GPU/step, tile {a.tile}, "
+            f"k={a.k}, multiplier 3, regime {regime} "
+            f"({'U[0,1)^N sorted by dim 0' if regime == 'R' else 'coherent tiles, spread 0.01'})")
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline (oracle/ndg_oracle.c, all host threads, bounded sample)
+# ------------------------------------------------------------------------------------------------
+def cpu_sample(a, mix_np, q, t, R, target_s):
+    """Time the C/OpenMP restatement on the first S tiles of the workload; return the extrapolated
+    full-batch step time. Fixed per-Gaussian costs (activation, projections, epilogue) are timed
+    once and counted once per step; per-tile costs (bounds, cull, forward, loss, backward) scale."""
+    import numpy as np
+
+    from oracle import c_oracle as CO
+    from oracle import ndg_oracle as O
+
+    CO.build()
+    threads = CO.max_threads()
+    om = O.OMixture(a.n_dims, 0, mix_np["params"].astype(np.float64), mix_np["child"].astype(np.float64),
+                    mix_np["has_child"], mix_np["frozen"])
+    T = q.shape[0] // a.tile
+
+    def run(S):
+        tm = {}
+        n = S * a.tile
+        t0 = time.perf_counter()
+        CO.step(om, q[:n], t[:n], R, tile=a.tile, n_total=q.shape[0], timings=tm)
+        wall = time.perf_counter() - t0
+        fixed = tm["eval_set"] + tm["project"] + tm["epilogue"]
+        return wall, fixed, wall - fixed
+
+    _, fixed1, var1 = run(1)
+    S = int(max(1, min(T, target_s / max(var1, 1e-6))))
+    wall, fixed, var = run(S)
+    est = fixed + var / S * T
+    return dict(step_s=est, sample_s=wall, tiles=S, threads=threads,
+                sample=f"first {S} of {T} tiles ({S * a.tile} queries) x all {om.G} Gaussians, "
+                       f"per-tile time extrapolated to the full batch + fixed per-Gaussian costs once")
+
+
+def reference_arm(a, rank, world):
+    """--impl reference: the reference's CPU path (C restatement, all host threads), rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import ndg_oracle as O
+    from paper_2405_20067_b200 import datasets as D
+    mix_np, _ = D.synthetic_mixture(a.n_dims, a.gaussians, seed=0, children=a.children)
+    q = D.synthetic_queries(a.n_dims, a.batch, seed=1, regime=a.regime, tile_size=a.tile)
+    t = D.synthetic_targets(a.batch, seed=3)
+    R = O.make_projection_set(a.n_dims, a.k, 2)
+    per = max(2.0, min(a.cpu_seconds, 150.0 / max(1, a.steps + a.warmup)))
+    times, info = [], None
+    for i in range(a.warmup + a.steps):
+        info = cpu_sample(a, mix_np, q, t, R, per)
+        if i >= a.warmup:
+            times.append(info["step_s"])
+    step_s = statistics.median(times)
+    v = a.batch / step_s
+    line = dict(metric=METRIC, value=v, unit="queries/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
+                ms_per_step=step_s * 1e3, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                data="synthetic", impl="reference",
+                config=dict(workload=workload_name(a, a.regime), n_dims=a.n_dims, gaussians=a.gaussians,
+                            batch_per_gpu=a.batch, tile=a.tile, k=a.k, multiplier=3.0, regime=a.regime),
+                cpu_baseline=dict(value=v, unit="queries/s", cores=info["threads"], kind="port",
+                                  sample=info["sample"], cpu=_cpu_model()),
+                e2e=dict(value=v, unit="queries/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+                note="reference ships no runnable implementation (SURVEY.md §0); timed: oracle/ndg_oracle.c "
+                     "(C/OpenMP restatement of SPEC.md, stand-in for the absent compiled _core)")
+    print(json.dumps(line), flush=True)
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(gpu_index), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"])
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 8]
+        os.unlink(self.f.name)
+        if not rows:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["no samples"])
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[5 + j].strip() == "Active"})
+        return dict(sm_mhz=statistics.median(sm), sm_max_mhz=mx, reasons=reasons, samples=len(rows),
+                    power_w_max=max(float(r[3]) for r in rows if r[3].strip() not in ("", "[N/A]")))
+
+
+# ------------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------------
+def fp32_peak(torch, K, dev):
+    """Measured FFMA rate of this GPU (TFLOP/s) -- the roofline denominator for K5 / K7."""
+    out = torch.empty(256, device=dev)
+    blocks, iters = 148 * 8, 4096
+    s = torch.cuda.current_stream()
+    import ctypes
+    for _ in range(2):
+        K.call("ndg_fp32_probe", ctypes.c_void_p(out.data_ptr()), blocks, iters, ctypes.c_void_p(s.cuda_stream))
+    best = 0.0
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        K.call("ndg_fp32_probe", ctypes.c_void_p(out.data_ptr()), blocks, iters, ctypes.c_void_p(s.cuda_stream))
+        b.record()
+        b.synchronize()
+        best = max(best, K.load().ndg_fp32_probe_flops(blocks, iters) / (a.elapsed_time(b) * 1e-3) / 1e12)
+    return best
+
+
+def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmup, measure_e2e):
+    import numpy as np
+
+    mix_np, s0 = D.synthetic_mixture(a.n_dims, a.gaussians, seed=0, children=a.children)
+    q = D.synthetic_queries(a.n_dims, a.batch, seed=1 + rank, regime=regime, tile_size=a.tile)
+    t = D.synthetic_targets(a.batch, seed=3 + rank)
+    mix = ndg.Mixture.from_arrays(a.n_dims, ndg.BRIGHTNESS, **mix_np, device=dev)
+    hp = ndg.HotPath(a.n_dims, k=a.k, multiplier=3.0, tile_size=a.tile, projection_seed=2, device=dev)
+    qd = torch.from_numpy(q).to(dev)
+    td = torch.from_numpy(t).to(dev)
+    grads = ndg.alloc_gradients(mix.G, mix.Gev, a.n_dims, dev)
+    state = ndg.new_adam_state(mix)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    n_total = a.batch * world
+    allreduce = (lambda flat: dist.all_reduce(flat)) if world > 1 else None
+    it = [0]
+
+    def step(queries, targets):
+        it[0] += 1
+        res = hp.fwd_bwd(mix, queries, targets, n_total=n_total, grads=grads, allreduce=allreduce)
+        ndg.adam_step(mix, grads, state, step=it[0])
+        return res
+
+    for _ in range(warmup):
+        res = step(qd, td)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) if rank == 0 else None
+    hp.enable_kernel_timing(True)
+    launches0 = K.launch_count
+    step_ms, kept, pairs = [], [], []
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for _ in range(steps):
+        flush.zero_()                                   # L2 flush, outside the timed interval
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = step(qd, td)
+        e1.record()
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        kept.append(res.kept_fraction)
+        pairs.append(res.candidates.n_pairs_tiles * a.tile)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = K.launch_count - launches0
+    clk = clocks.stop() if clocks else None
+    fwd_ms = statistics.mean(hp.kernel_ms("forward"))
+    bwd_ms = statistics.mean(hp.kernel_ms("backward"))
+    hp.enable_kernel_timing(False)
+    total_ms = sum(step_ms)
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt)
+    out = dict(total_ms=total_ms, ms_per_step=total_ms / steps, value=a.batch * world * steps / (total_ms * 1e-3),
+               kept=statistics.mean(kept), pairs=statistics.mean(pairs), fwd_ms=fwd_ms, bwd_ms=bwd_ms,
+               launches=launches, clocks=clk, loss=res.loss, sigma0=s0)
+
+    if measure_e2e:
+        qh = torch.from_numpy(q).pin_memory()
+        th = torch.from_numpy(t).pin_memory()
+        e2e_ms = []
+        for i in range(warmup + steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.zero_()
+            e0.record()
+            qd2 = qh.to(dev, non_blocking=True)
+            td2 = th.to(dev, non_blocking=True)
+            res = step(qd2, td2)                       # fwd_bwd reads the loss back to the host
+            e1.record()
+            e1.synchronize()
+            if i >= warmup:
+                e2e_ms.append(e0.elapsed_time(e1))
+        tot = sum(e2e_ms)
+        if world > 1:
+            tt = torch.tensor([tot], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tot = float(tt)
+        out["e2e"] = dict(value=a.batch * world * steps / (tot * 1e-3), unit="queries/s",
+                          h2d_bytes_per_step=int(q.nbytes + t.nbytes), d2h_bytes_per_step=8 + 32,
+                          ms_per_step=tot / steps)
+    return out, (mix_np, q, t, hp.ps.vectors)
+
+
+def our_arm(a, rank, world):
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2405_20067_b200 as ndg
+    from paper_2405_20067_b200 import datasets as D
+    from paper_2405_20067_b200 import kernels as K
+
+    peak = fp32_peak(torch, K, dev)
+    main, (mix_np, q, t, R) = run_regime(a, a.regime, torch, ndg, D, K, dist, rank, world, dev, a.steps, a.warmup,
+                                         not a.no_e2e)
+    secondary = None
+    if not a.no_secondary:
+        other = "C" if a.regime == "R" else "R"
+        s, _ = run_regime(a, other, torch, ndg, D, K, dist, rank, world, dev, max(3, a.steps // 2), 3, False)
+        secondary = {f"regime_{other}": dict(value=s["value"], unit="queries/s", ms_per_step=s["ms_per_step"],
+                                             kept_fraction=s["kept"], pairs_per_step=s["pairs"],
+                                             workload=workload_name(a, other),
+                                             fp32_frac_step=s["pairs"] * ndg.kept_pairs_flops(a.n_dims)
+                                             / (s["ms_per_step"] * 1e-3) / 1e12 / peak)}
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    n = a.n_dims
+    f_fwd, f_bwd = n * n + 3 * n + 8, 2 * n * n + 6 * n + 14
+    pairs = main["pairs"]
+    kern = {
+        "forward": dict(ms=main["fwd_ms"], tflops=pairs * f_fwd / (main["fwd_ms"] * 1e-3) / 1e12),
+        "backward": dict(ms=main["bwd_ms"], tflops=pairs * f_bwd / (main["bwd_ms"] * 1e-3) / 1e12),
+    }
+    for v in kern.values():
+        v["frac_of_measured_fp32"] = v["tflops"] / peak
+        v["share_of_step"] = v["ms"] / main["ms_per_step"]
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(f"{dom}:N{n}:G{a.gaussians}:B{a.batch}:{a.regime}")
+    except (OSError, ValueError):
+        pass
+    step_tflops = pairs * ndg.kept_pairs_flops(n) / (main["ms_per_step"] * 1e-3) / 1e12
+    line = dict(
+        metric=METRIC, value=main["value"], unit="queries/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
+        ms_per_step=main["ms_per_step"], higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f32",
+        data="synthetic (seeded NumPy PCG64 mixture / queries / targets of the named shape)",
+        config=dict(workload=workload_name(a, a.regime), n_dims=n, gaussians=a.gaussians,
+                    evaluated_gaussians=a.gaussians * (2 if a.children else 1), batch_per_gpu=a.batch,
+                    global_batch=a.batch * world, tile=a.tile, k=a.k, multiplier=3.0, regime=a.regime,
+                    kept_fraction=main["kept"], pairs_per_step=pairs, sigma0=main["sigma0"],
+                    l2="flushed before every timed step (256 MiB write, outside the timed interval)",
+                    parallelism=f"dp{world} (tiles sharded, mixture replicated, 1 NCCL allreduce/step)"),
+        roofline=dict(bound="fp32", kernel=dom, achieved=kern[dom]["tflops"], peak=peak, unit="TFLOP/s",
+                      frac=kern[dom]["tflops"] / peak, traffic=traffic,
+                      peak_source="measured FFMA probe (ndg_fp32_probe) on this GPU; MEASURED_PEAKS.json has no "
+                                  "FP32 entry",
+                      peak_nominal=NOMINAL_FP32_TFLOPS, frac_of_nominal=kern[dom]["tflops"] / NOMINAL_FP32_TFLOPS,
+                      flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n)),
+                      step_achieved=step_tflops, step_frac=step_tflops / peak),
+        kernels=kern, gpu_launches=main["launches"], clocks=main["clocks"], loss=main["loss"],
+    )
+    if "e2e" in main:
+        line["e2e"] = main["e2e"]
+    if secondary:
+        line["secondary"] = secondary
+    if world == 1 and not a.no_cpu_baseline:
+        info = cpu_sample(a, mix_np, q, t, R, a.cpu_seconds)
+        line["cpu_baseline"] = dict(value=a.batch / info["step_s"], unit="queries/s", cores=info["threads"],
+                                    kind="port", sample=info["sample"], cpu=_cpu_model(),
+                                    sample_seconds=info["sample_s"])
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if a.impl == "reference":
+        reference_arm(a, rank, world)
+    else:
+        our_arm(a, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -144,6 +144,11 @@ int ndg_adam(int n, int64_t rows, float* params, const float* grad, float* m1, f
              int step, float lr_mean, float lr_chol, float lr_color, float lr_amp, float beta1, float beta2,
              float eps, void* stream);
 
+/* FP32-pipe peak probe (roofline denominator for K5 / K7; not part of the reference interface):
+ * `blocks` CTAs of 256 threads, each running 8 independent FFMA chains for 16 * iters steps. */
+int ndg_fp32_probe(float* out, int blocks, int iters, void* stream);
+double ndg_fp32_probe_flops(int blocks, int iters);
+
 #ifdef __cplusplus
 }
 #endif

@@ -164,6 +164,25 @@ class HotPath:
         self.tile = int(tile_size)
         self.eps = float(eps)
         self.status = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self.events = None   # when a dict: {"forward": [(start, end), ...], "backward": [...]} CUDA events
+
+    def enable_kernel_timing(self, on: bool = True):
+        """Record CUDA events on the launching stream around the K5 and K7 launches."""
+        self.events = {"forward": [], "backward": []} if on else None
+
+    def _ev(self, name, when):
+        if self.events is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        if when == 0:
+            self.events[name].append([e, None])
+        else:
+            self.events[name][-1][1] = e
+
+    def kernel_ms(self, name):
+        """Per-launch durations (ms) of the recorded launches of K5 ("forward") / K7 ("backward")."""
+        return [a.elapsed_time(b) for a, b in self.events[name]]
 
     # -- K1 --------------------------------------------------------------------------------
     def activate(self, mix: Mixture) -> EvalRecords:
@@ -244,8 +263,10 @@ class HotPath:
         if targets is not None:
             qrec = torch.empty(B, self.L["qrec"], dtype=torch.float32, device=self.device)
             loss_part = torch.empty(T, dtype=torch.float64, device=self.device)
+        self._ev("forward", 0)
         K.call("ndg_forward", self.n, B, self.tile, _p(queries), _p(targets), _p(recs.rec), _p(cl.offsets), _p(cl.idx),
                self.eps, int(n_total or B), _p(pred), _p(qrec), _p(loss_part), _stream())
+        self._ev("forward", 1)
         return pred, qrec, loss_part
 
     def finalize_loss(self, loss_part) -> torch.Tensor:
@@ -257,8 +278,10 @@ class HotPath:
     def backward(self, mix: Mixture, recs: EvalRecords, cl: CandidateLists, qrec, grads: GradientBuffer):
         B = int(qrec.shape[0])
         accum = torch.zeros(recs.Gev, self.L["acc"], dtype=torch.float64, device=self.device)
+        self._ev("backward", 0)
         K.call("ndg_backward", self.n, B, self.tile, _p(qrec), _p(recs.rec), _p(cl.offsets), _p(cl.idx),
                _p(cl.chunk_offsets), cl.n_chunks, _p(accum), _stream())
+        self._ev("backward", 1)
         K.call("ndg_epilogue", self.n, mix.G, recs.Gev, mix.amp_mode, _p(mix.params), _p(mix.child), _p(mix.flags),
                _p(recs.eflags), _p(recs.chol64), _p(accum), _p(grads.params), _p(grads.child), _p(grads.stats),
                _p(self.status), _stream())

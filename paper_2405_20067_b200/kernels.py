@@ -41,6 +41,8 @@ SIGNATURES = {
     "ndg_backward": [_I, _L, _I, _P, _P, _P, _P, _P, _L, _P, _P],
     "ndg_epilogue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "ndg_adam": [_I, _L, _P, _P, _P, _P, _P, _I, _F, _F, _F, _F, _F, _F, _F, _P],
+    "ndg_fp32_probe": [_P, _I, _I, _P],
+    "ndg_fp32_probe_flops": [_I, _I],
 }
 
 ERRORS = {0: "NDG_OK", 1: "NDG_ERR_INVALID_PARAMETER", 2: "NDG_ERR_NONFINITE_GRADIENT",
@@ -66,7 +68,7 @@ def load():
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
-        fn.restype = C.c_char_p if name == "ndg_last_error" else C.c_int
+        fn.restype = {"ndg_last_error": C.c_char_p, "ndg_fp32_probe_flops": C.c_double}.get(name, C.c_int)
     _lib = lib
     return lib
 
@@ -75,10 +77,20 @@ class NdgLaunchError(RuntimeError):
     pass
 
 
+# entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
+LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_scan_counts",
+             "ndg_cull_compact", "ndg_forward", "ndg_loss_finalize", "ndg_backward", "ndg_epilogue", "ndg_adam",
+             "ndg_fp32_probe"}
+launch_count = 0
+
+
 def call(name: str, *args):
     """Invoke an entry point; a nonzero launch code raises with the library's error string."""
+    global launch_count
     lib = load()
     rc = getattr(lib, name)(*args)
+    if name in LAUNCHING:
+        launch_count += 1
     if rc != 0:
         msg = lib.ndg_last_error().decode(errors="replace")
         raise NdgLaunchError(f"{name} failed: {ERRORS.get(rc, rc)} {msg}")
