@@ -18,9 +18,15 @@ using namespace ndg;
 namespace {
 
 constexpr int kBwdThreads = kBwdChunk;
+#ifndef NDG_BWD_PIPE
+#define NDG_BWD_PIPE 0
+#endif
+#ifndef NDG_BWD_MINB
+#define NDG_BWD_MINB 3
+#endif
 
 template <int N>
-__global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? 3 : 1))
+__global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     backward_kernel(int64_t T, int tile, const float* __restrict__ qrec, const float* __restrict__ rec,
                     const int64_t* __restrict__ offsets, const int32_t* __restrict__ idx,
                     const int64_t* __restrict__ chunk_off, double* __restrict__ accum) {
@@ -79,6 +85,61 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? 3 : 1))
     for (int i = 0; i < N; ++i) tv[i] = 0.f;
     gA[0] = gA[1] = gA[2] = 0.f;
 
+#if NDG_BWD_PIPE
+    // software-pipelined: z~ of query q+1 is computed while query q's outer products accumulate
+    float zn[N], sn;
+    auto solve = [&](int q, float* z, float& s2, float* dq) {
+        const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
+        float xq[QS];
+#pragma unroll
+        for (int v = 0; v < QS / 4; ++v) {
+            const float4 x = q4[v];
+            xq[4 * v] = x.x;
+            xq[4 * v + 1] = x.y;
+            xq[4 * v + 2] = x.z;
+            xq[4 * v + 3] = x.w;
+        }
+        s2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb(N) + i]);
+#pragma unroll
+            for (int k = 0; k < i; ++k) acc = fmaf(r[rec_lu(N) + tri_s(i, k)], z[k], acc);
+            z[i] = acc;
+            s2 = fmaf(acc, acc, s2);
+        }
+        dq[0] = xq[N];
+        dq[1] = xq[N + 1];
+        dq[2] = xq[N + 2];
+        dq[3] = xq[N + 3];
+    };
+    float dqn[4];
+    solve(0, zn, sn, dqn);
+    for (int q = 0; q < tile; ++q) {
+        float z[N], dq[4];
+        const float s2 = sn;
+#pragma unroll
+        for (int i = 0; i < N; ++i) z[i] = zn[i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dq[i] = dqn[i];
+        if (q + 1 < tile) solve(q + 1, zn, sn, dqn);
+        const float g = ex2_neg(s2);
+        const float h = fmaf(dq[2], r[A0 + 2], fmaf(dq[1], r[A0 + 1], dq[0] * r[A0]));
+        const float wgt = g * h;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const float u = wgt * z[i];
+            tv[i] += u;
+#pragma unroll
+            for (int j = 0; j <= i; ++j) S[tri(i, j)] = fmaf(u, z[j], S[tri(i, j)]);
+        }
+        gA[0] = fmaf(g, dq[0], gA[0]);
+        gA[1] = fmaf(g, dq[1], gA[1]);
+        gA[2] = fmaf(g, dq[2], gA[2]);
+        ls = fmaf(g, dq[3], ls);
+        px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
+    }
+#else
     for (int q = 0; q < tile; ++q) {
         float xq[QS];
         const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
@@ -117,6 +178,8 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? 3 : 1))
         ls = fmaf(g, ell, ls);
         px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
     }
+
+#endif
 
     double* out = accum + e * A;
 #pragma unroll

@@ -16,13 +16,26 @@ using namespace ndg;
 
 namespace {
 
-constexpr int kFwdThreads = 128;
-constexpr int kQPT = 2;                     // queries per thread -> 256 queries per pass
 constexpr int kChunk = 32;                  // candidate records per ring stage (one per lane of warp 0)
-constexpr int kStages = 2;
 
-template <int N>
-__global__ void __launch_bounds__(kFwdThreads, 4)
+// Launch shape per N: QPT queries per thread x NT threads = 256 queries per pass (one tile).
+#ifndef NDG_FWD_QPT
+#define NDG_FWD_QPT 4
+#endif
+template <int N> struct FwdCfg { static constexpr int QPT = NDG_FWD_QPT, NT = 256 / NDG_FWD_QPT, STAGES = 2; };
+template <> struct FwdCfg<11> { static constexpr int QPT = 2, NT = 128, STAGES = 4; };
+template <> struct FwdCfg<12> { static constexpr int QPT = 2, NT = 128, STAGES = 4; };
+template <> struct FwdCfg<13> { static constexpr int QPT = 2, NT = 128, STAGES = 4; };
+template <> struct FwdCfg<14> { static constexpr int QPT = 2, NT = 128, STAGES = 3; };
+template <> struct FwdCfg<15> { static constexpr int QPT = 2, NT = 128, STAGES = 3; };
+template <> struct FwdCfg<16> { static constexpr int QPT = 2, NT = 128, STAGES = 3; };
+
+// Ring protocol (no CTA-wide barrier in the loop): full[s] completes when the TMA engine has
+// landed the stage's records (expect_tx by lane 0 of warp 0); empty[s] completes when every warp
+// has finished reading the stage (one arrive per warp). Only warp 0 (the producer) ever waits on
+// empty[s], just before refilling it; consumer warps never wait on each other.
+template <int N, int QPT, int NT, int STAGES>
+__global__ void __launch_bounds__(NT)
     forward_kernel(int tile, const float* __restrict__ queries, const float* __restrict__ targets,
                    const float* __restrict__ rec, const int64_t* __restrict__ offsets,
                    const int32_t* __restrict__ idx, float eps, double inv3n, float* __restrict__ pred,
@@ -30,9 +43,10 @@ __global__ void __launch_bounds__(kFwdThreads, 4)
     constexpr int RS = rec_floats(N);
     constexpr int QS = qrec_floats(N);
     constexpr int A0 = rec_a(N);
-    extern __shared__ __align__(128) float s_rec[];           // [kStages][kChunk][RS]
-    __shared__ __align__(8) uint64_t full_bar[kStages];
-    __shared__ double s_loss[kFwdThreads / 32];
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(128) float s_rec[];           // [STAGES][kChunk][RS]
+    __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+    __shared__ double s_loss[NW];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t t = blockIdx.x;
@@ -40,12 +54,15 @@ __global__ void __launch_bounds__(kFwdThreads, 4)
     const int nchunks = (int)((end - beg + kChunk - 1) / kChunk);
 
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], NW);
+        }
         fence_mbar_init();
     }
     __syncthreads();
 
-    // producer: warp 0, lane l copies candidate l of chunk c into stage s
+    // producer (warp 0): lane l copies candidate l of chunk c into stage s
     auto issue = [&](int c, int s) {
         const int64_t cb = beg + (int64_t)c * kChunk;
         const int n_in = (int)imin64(kChunk, end - cb);
@@ -58,13 +75,13 @@ __global__ void __launch_bounds__(kFwdThreads, 4)
     };
 
     double loss_acc = 0.0;
-    uint32_t phase_ctr = 0;   // ring position across passes (barrier parity bookkeeping)
-    for (int q0 = 0; q0 < tile; q0 += kFwdThreads * kQPT) {
-        float x[kQPT][N], p[kQPT][3];
-        bool valid[kQPT];
+    uint32_t ring = 0;   // ring position across passes (stage = ring % STAGES, parity = ring / STAGES)
+    for (int q0 = 0; q0 < tile; q0 += NT * QPT) {
+        float x[QPT][N], p[QPT][3];
+        bool valid[QPT];
 #pragma unroll
-        for (int j = 0; j < kQPT; ++j) {
-            const int qi = q0 + tid + j * kFwdThreads;
+        for (int j = 0; j < QPT; ++j) {
+            const int qi = q0 + tid + j * NT;
             valid[j] = qi < tile;
             const float* src = queries + (t * tile + qi) * N;
 #pragma unroll
@@ -72,12 +89,16 @@ __global__ void __launch_bounds__(kFwdThreads, 4)
             p[j][0] = p[j][1] = p[j][2] = 0.f;
         }
         if (warp == 0) {
-            for (int c = 0; c < kStages && c < nchunks; ++c) issue(c, (int)((phase_ctr + c) % kStages));
+            for (int c = 0; c < STAGES && c < nchunks; ++c) {
+                const uint32_t pos = ring + c;
+                if (pos >= STAGES) mbar_wait(&empty_bar[pos % STAGES], ((pos / STAGES) - 1) & 1);
+                issue(c, (int)(pos % STAGES));
+            }
         }
         for (int c = 0; c < nchunks; ++c) {
-            const uint32_t pos = phase_ctr + c;
-            const int s = (int)(pos % kStages);
-            mbar_wait(&full_bar[s], (pos / kStages) & 1);
+            const uint32_t pos = ring + c;
+            const int s = (int)(pos % STAGES);
+            mbar_wait(&full_bar[s], (pos / STAGES) & 1);
             const int n_in = (int)imin64(kChunk, end - beg - (int64_t)c * kChunk);
             const float* sr = s_rec + s * kChunk * RS;
             for (int ci = 0; ci < n_in; ++ci) {
@@ -92,7 +113,7 @@ __global__ void __launch_bounds__(kFwdThreads, 4)
                     r[4 * v + 3] = w.w;
                 }
 #pragma unroll
-                for (int j = 0; j < kQPT; ++j) {
+                for (int j = 0; j < QPT; ++j) {
                     float z[N];
                     float s2 = 0.f;
 #pragma unroll
@@ -109,15 +130,19 @@ __global__ void __launch_bounds__(kFwdThreads, 4)
                     p[j][2] = fmaf(g, r[A0 + 2], p[j][2]);
                 }
             }
-            __syncthreads();   // every warp is done with stage s
-            if (warp == 0 && c + kStages < nchunks) issue(c + kStages, s);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[s]);       // this warp is done with stage s
+            if (warp == 0 && c + STAGES < nchunks) {
+                mbar_wait(&empty_bar[s], (pos / STAGES) & 1);  // all warps done with stage s
+                issue(c + STAGES, s);
+            }
         }
-        phase_ctr += (uint32_t)nchunks;
+        ring += (uint32_t)nchunks;
 
 #pragma unroll
-        for (int j = 0; j < kQPT; ++j) {
+        for (int j = 0; j < QPT; ++j) {
             if (!valid[j]) continue;
-            const int64_t b = t * tile + q0 + tid + j * kFwdThreads;
+            const int64_t b = t * tile + q0 + tid + j * NT;
             pred[b * 3] = p[j][0];
             pred[b * 3 + 1] = p[j][1];
             pred[b * 3 + 2] = p[j][2];
@@ -147,7 +172,7 @@ __global__ void __launch_bounds__(kFwdThreads, 4)
         __syncthreads();
         if (tid == 0) {
             double s = 0.0;
-            for (int w = 0; w < kFwdThreads / 32; ++w) s += s_loss[w];
+            for (int w = 0; w < NW; ++w) s += s_loss[w];
             loss_partial[t] = s;
         }
     }
@@ -157,15 +182,17 @@ template <int N>
 int launch_forward(int64_t B, int tile, const float* q, const float* tgt, const float* rec, const int64_t* off,
                    const int32_t* idx, float eps, int64_t n_total, float* pred, float* qrec, double* lp,
                    cudaStream_t st) {
+    using C = FwdCfg<N>;
     const int64_t T = B / tile;
-    const size_t smem = sizeof(float) * kStages * kChunk * rec_floats(N);
+    const size_t smem = sizeof(float) * C::STAGES * kChunk * rec_floats(N);
+    auto kern = forward_kernel<N, C::QPT, C::NT, C::STAGES>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(forward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    forward_kernel<N><<<(unsigned)T, kFwdThreads, smem, st>>>(tile, q, tgt, rec, off, idx, eps,
-                                                              1.0 / (3.0 * (double)n_total), pred, qrec, lp);
+    kern<<<(unsigned)T, C::NT, smem, st>>>(tile, q, tgt, rec, off, idx, eps, 1.0 / (3.0 * (double)n_total), pred,
+                                           qrec, lp);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }

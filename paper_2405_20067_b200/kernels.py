@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libndg.so")
+LIB_PATH = os.environ.get("NDG_LIB") or os.path.join(_HERE, "libndg.so")   # NDG_LIB: tuning builds only
 
 _P = C.c_void_p
 _I = C.c_int
