@@ -148,6 +148,24 @@ def alloc_gradients(G: int, Gev: int, n: int, device) -> GradientBuffer:
     return GradientBuffer(flat, gp, gc, st, flat[o:o + 2])
 
 
+def decode_status(st, G: int, n: int) -> int:
+    """Map the device status word (include/ndg.h ndg_status) onto the reference's exceptions
+    (errors.py:8-33); returns the degenerate-Gaussian count when there is no error."""
+    R = raw_width(n)
+    for slot, cls in ((0, InvalidParameterError), (1, NonFiniteGradientError)):
+        if st[slot] != 0:
+            key = _INT64_MAX - int(st[slot])
+            which = "child" if key >= G * R else "parent"
+            comp, entry = divmod(key % (G * R), R)
+            blk = 0 if entry < n else 1 if entry < n + n_chol(n) else 2 if entry < n + n_chol(n) + 3 else 3
+            if cls is InvalidParameterError:
+                raise InvalidParameterError(f"non-finite raw parameter ({which} row, block {_BLOCKS[blk]})",
+                                            component=int(comp), block=_BLOCKS[blk], entry=int(entry))
+            raise NonFiniteGradientError(f"non-finite gradient ({which} row, block {_BLOCKS[blk]})",
+                                         component=int(comp), block=_BLOCKS[blk], batch_index=-1)
+    return int(st[2])
+
+
 class HotPath:
     """One object per (device, N). Each method is one stage; `fwd_bwd` chains them."""
 
@@ -293,21 +311,7 @@ class HotPath:
 
     def check_status(self, mix: Mixture, host_status=None):
         st = (self.status.cpu() if host_status is None else host_status).tolist()
-        R = raw_width(self.n)
-        for slot, cls in ((0, InvalidParameterError), (1, NonFiniteGradientError)):
-            if st[slot] != 0:
-                key = _INT64_MAX - st[slot]
-                which = "child" if key >= mix.G * R else "parent"
-                key %= mix.G * R
-                comp, entry = divmod(key, R)
-                n = self.n
-                blk = 0 if entry < n else 1 if entry < n + n_chol(n) else 2 if entry < n + n_chol(n) + 3 else 3
-                if cls is InvalidParameterError:
-                    raise InvalidParameterError(f"non-finite raw parameter ({which} row, block {_BLOCKS[blk]})",
-                                                component=int(comp), block=_BLOCKS[blk], entry=int(entry))
-                raise NonFiniteGradientError(f"non-finite gradient ({which} row, block {_BLOCKS[blk]})",
-                                             component=int(comp), block=_BLOCKS[blk], batch_index=-1)
-        return int(st[2])
+        return decode_status(st, mix.G, self.n)
 
     # -- whole step ------------------------------------------------------------------------
     def fwd_bwd(self, mix: Mixture, queries, targets, *, cull: bool = True, n_total=None, grads=None,
