@@ -4,7 +4,7 @@
 Only what the hot path needs: the tile definition of sample_batch (queries sorted by the first
 dimension, contiguous tiles of tile_size) and the synthetic mixture / query /
 target generators the benchmark and the fit loop use. The generators are host-side NumPy (not on
-the timed path); tests/test_datasets.py checks they match the oracle's copies value for value.
+the timed path); tests/test_cpu_infra.py checks they match the oracle's copies value for value.
 """
 from __future__ import annotations
 
@@ -95,3 +95,75 @@ def synthetic_queries(n: int, B: int, seed: int = 1, *, regime: str = "R", tile_
 
 def synthetic_targets(B: int, seed: int = 3) -> np.ndarray:
     return np.random.default_rng(seed).random((B, 3)).astype(np.float32)
+
+
+# ------------------------------------------------------------------------------------------------
+# device-side batch sampling and procedural targets
+# ------------------------------------------------------------------------------------------------
+class GmmOracleTarget:
+    """gmm_oracle_target: a hidden mixture of the exact model family; targets are
+    its exact (culling disabled) evaluation at the queries, on the GPU."""
+
+    def __init__(self, seed: int, n_dims: int, n_components: int, amp_mode: int = BRIGHTNESS, device=None,
+                 sigma0: float | None = None):
+        import torch
+        from .engine import HotPath
+        from .gmm import Mixture
+        self.n_dims = n_dims
+        rows, self.sigma0 = synthetic_mixture(n_dims, n_components, seed=seed + 7919, amp_mode=amp_mode,
+                                              sigma0=sigma0 if sigma0 is not None else 0.15)
+        rows["params"][:, -1] = np.log(0.3) if amp_mode == BRIGHTNESS else 0.0
+        self.mixture = Mixture.from_arrays(n_dims, amp_mode, **rows, device=device)
+        self.hp = HotPath(n_dims, tile_size=256, device=self.mixture.device)
+        self._torch = torch
+
+    def __call__(self, queries):
+        return self.hp.evaluate(self.mixture, queries, cull=False)
+
+
+class ShadingToyTarget:
+    """shading_toy_target: analytic shading-like function of
+    position(3) | view direction(3) | albedo(3) | roughness(1) (first N of these roles, N in 4..10):
+    a diffuse term smooth in position and modulated by albedo, plus a glossy cosine-power lobe around
+    a position-dependent reflection direction whose exponent falls to its minimum at roughness 1."""
+
+    def __init__(self, seed: int, n_dims: int):
+        if not 4 <= n_dims <= 10:
+            raise ValueError("shading toy needs 4 <= N <= 10")
+        rng = np.random.default_rng(seed)
+        self.n_dims = n_dims
+        self.freq = rng.uniform(1.0, 2.0, 3)
+        self.phase = rng.uniform(0, 2 * np.pi, 3)
+
+    def __call__(self, q):
+        import torch
+        n = self.n_dims
+        pos = q[:, :3]
+        f = torch.tensor(self.freq, device=q.device, dtype=q.dtype)
+        ph = torch.tensor(self.phase, device=q.device, dtype=q.dtype)
+        shade = 0.55 + 0.45 * torch.sin(2 * np.pi * f * pos + ph).prod(dim=1, keepdim=True)
+        alb = q[:, 6:9] if n >= 9 else torch.full((q.shape[0], 3), 0.6, device=q.device, dtype=q.dtype)
+        rough = q[:, 9:10] if n >= 10 else torch.full((q.shape[0], 1), 0.5, device=q.device, dtype=q.dtype)
+        if n >= 6:
+            v = 2.0 * q[:, 3:6] - 1.0
+        else:
+            v = torch.cat([2.0 * q[:, 3:n] - 1.0, torch.ones(q.shape[0], 6 - n, device=q.device, dtype=q.dtype)], 1)
+        v = v / v.norm(dim=1, keepdim=True).clamp_min(1e-6)
+        refl = torch.stack([torch.sin(2 * np.pi * pos[:, 0]), torch.cos(2 * np.pi * pos[:, 1]),
+                            0.5 + pos[:, 2]], 1)
+        refl = refl / refl.norm(dim=1, keepdim=True)
+        expo = 2.0 + 40.0 * (1.0 - rough)
+        lobe = (v * refl).sum(1, keepdim=True).clamp_min(0.0) ** expo
+        return (alb * shade * 0.6 + 0.4 * lobe).to(torch.float32)
+
+
+def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, generator, device):
+    """SPEC.md:440-448 on the device: fresh uniform queries, stable-sorted by the first (position)
+    dimension into contiguous tiles, exact targets. batch_size must be a multiple of tile_size."""
+    import torch
+    if batch_size % tile_size:
+        raise ValueError("batch_size must be a multiple of tile_size (SPEC.md:441)")
+    q = torch.rand(batch_size, n_dims, generator=generator, device=device)
+    order = torch.sort(q[:, 0], stable=True).indices
+    q = q[order].contiguous()
+    return q, target(q).contiguous()

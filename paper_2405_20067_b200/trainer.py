@@ -1,0 +1,262 @@
+"""Fit loop with optimizer-controlled refinement (reference module trainer).
+
+One iteration: sample batch → tile → cull → forward → loss → backward → Adam, i.e. one
+`HotPath.fwd_bwd` (K1-K8, plus the single NCCL all_reduce when data-parallel) and one `adam_step`
+(K9) on the device. Refinement events run between iterations on the host ("single
+threaded between iterations") every `phase_length` iterations after `warmup_phases` phases:
+check_materialize → materialize → spawn_children, and components whose activated
+amplitude stayed below t/100 for a whole phase are frozen out. New rows and children
+start with zeroed Adam moments.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import datasets as D
+from .engine import HotPath, adam_step, alloc_gradients, new_adam_state
+from .errors import TrainingAborted
+from .gmm import BRIGHTNESS, FLAG_CHILD, FLAG_FROZEN, Mixture, n_chol, raw_slices, raw_width, tri
+
+
+@dataclass
+class TrainConfig:
+    """SPEC.md:309-318 with the ledger defaults."""
+    iterations: int = 1000
+    phase_length: int = 300
+    warmup_phases: int = 1
+    materialize_threshold: float | None = None      # default: 0.1 opacity / 0.01 brightness
+    lr_mean: float = 2e-3
+    lr_chol: float = 5e-3
+    lr_color: float = 1e-2
+    lr_amp: float = 1e-2
+    beta1: float = 0.9
+    beta2: float = 0.999
+    adam_eps: float = 1e-8
+    batch_size: int = 1 << 16
+    tile_size: int = 256
+    seed: int = 0
+    k: int = 16
+    multiplier: float = 3.0
+    loss_eps: float = 0.01
+    cull: bool = True
+    n_components: int = 256
+    amp_mode: int = BRIGHTNESS
+
+    def threshold(self) -> float:
+        return self.materialize_threshold if self.materialize_threshold is not None else \
+            D.default_threshold(self.amp_mode)
+
+
+@dataclass
+class MetricsRow:
+    """metrics.csv row: iteration,loss,n_components,culled_fraction,ms_per_iter."""
+    iteration: int
+    loss: float
+    n_components: int
+    culled_fraction: float
+    ms_per_iter: float
+
+
+@dataclass
+class TrainResult:
+    mixture: Mixture
+    metrics: list = field(default_factory=list)
+    events: list = field(default_factory=list)
+
+
+# ------------------------------------------------------------------------------------------------
+# activation helpers for the refinement events (host, float64, between iterations)
+# ------------------------------------------------------------------------------------------------
+def _sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def _activate(chol_raw, n):
+    L = np.zeros(chol_raw.shape[:-1] + (n, n))
+    for i in range(n):
+        for j in range(i + 1):
+            r = chol_raw[..., tri(i, j)]
+            L[..., i, j] = np.exp(r) if i == j else 2.0 * _sigmoid(r) - 1.0
+    return L
+
+
+def _inverse_activate(L, n, clamp=1.0 - 1e-6):
+    raw = np.zeros(L.shape[:-2] + (n_chol(n),))
+    clamped = 0
+    for i in range(n):
+        for j in range(i + 1):
+            v = L[..., i, j]
+            if i == j:
+                raw[..., tri(i, j)] = np.log(v)
+            else:
+                vc = np.clip(v, -clamp, clamp)          # clamp to +-(1 - 1e-6) and log it
+                clamped += int(np.count_nonzero(vc != v))
+                s = (vc + 1.0) / 2.0
+                raw[..., tri(i, j)] = np.log(s) - np.log1p(-s)
+    return raw, clamped
+
+
+def _amp(raw, mode):
+    return np.exp(raw) if mode == BRIGHTNESS else _sigmoid(raw)
+
+
+def spawn_rows(n, count, mode, t, rng):
+    """spawn_children: U = I, m_u = 0, color_raw in +-0.1, activated amp = t/10."""
+    ms, cs, cols, amp = raw_slices(n)
+    rows = np.zeros((count, raw_width(n)), np.float32)
+    rows[:, cols] = rng.uniform(-0.1, 0.1, (count, 3))
+    rows[:, amp] = D.amp_inverse(t / 10.0, mode)
+    return rows
+
+
+def initial_mixture(cfg: TrainConfig, n_dims: int, points: torch.Tensor, device) -> Mixture:
+    """Means from dataset points, per-dimension sigma = half the mean nearest-neighbour distance,
+    zero off-diagonals; neutral colour; amplitude 0.5 of the brightness scale."""
+    pts = points[: cfg.n_components].double().cpu().numpy()
+    s0 = D.nn_sigma0(pts)
+    ms, cs, cols, amp = raw_slices(n_dims)
+    rows = np.zeros((cfg.n_components, raw_width(n_dims)), np.float32)
+    rows[:, ms] = pts
+    for i in range(n_dims):
+        rows[:, cs.start + tri(i, i)] = math.log(max(s0, 1e-3))
+    rows[:, amp] = D.amp_inverse(0.5 if cfg.amp_mode == BRIGHTNESS else 0.5, cfg.amp_mode)
+    return Mixture.from_arrays(n_dims, cfg.amp_mode, rows, device=device)
+
+
+class Trainer:
+    """Holds the device state of one fit: mixture, Adam moments, freeze counters, hot path."""
+
+    def __init__(self, cfg: TrainConfig, target, n_dims: int, *, mixture: Mixture | None = None, device=None,
+                 allreduce=None, rank: int = 0, world: int = 1):
+        self.cfg, self.target, self.n = cfg, target, n_dims
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.gen = torch.Generator(device=self.device)
+        self.gen.manual_seed(cfg.seed * 1000003 + rank)
+        self.rng = np.random.default_rng(cfg.seed)
+        self.allreduce, self.rank, self.world = allreduce, rank, world
+        if mixture is None:
+            q0, _ = D.sample_batch(target, n_dims, max(cfg.tile_size, cfg.n_components), 1, self._init_gen(),
+                                   self.device)
+            mixture = initial_mixture(cfg, n_dims, q0[torch.randperm(q0.shape[0], generator=self._init_gen(),
+                                                                     device=self.device)], self.device)
+        self.mix = mixture
+        self.hp = HotPath(n_dims, k=cfg.k, multiplier=cfg.multiplier, tile_size=cfg.tile_size, eps=cfg.loss_eps,
+                          projection_seed=cfg.seed, device=self.device)
+        self.state = new_adam_state(self.mix)
+        self.low_count = torch.zeros(self.mix.G, dtype=torch.int32, device=self.device)
+        self.step_no = 0
+        self.last_good = self.mix.clone()
+
+    def _init_gen(self):
+        g = torch.Generator(device=self.device)
+        g.manual_seed(self.cfg.seed)           # identical initial mixture on every rank
+        return g
+
+    # -- one iteration -----------------------------------------------------------------------
+    def iteration(self) -> MetricsRow:
+        cfg = self.cfg
+        t0 = time.perf_counter()
+        q, tg = D.sample_batch(self.target, self.n, cfg.batch_size, cfg.tile_size, self.gen, self.device)
+        res = self.hp.fwd_bwd(self.mix, q, tg, cull=cfg.cull, n_total=cfg.batch_size * self.world,
+                              allreduce=self.allreduce)
+        if not math.isfinite(res.loss):
+            self.mix = self.last_good.clone()
+            raise TrainingAborted(f"non-finite loss at iteration {self.step_no}", iteration=self.step_no)
+        self.step_no += 1
+        adam_step(self.mix, res.grads, self.state, self.step_no,
+                  lr=(cfg.lr_mean, cfg.lr_chol, cfg.lr_color, cfg.lr_amp), betas=(cfg.beta1, cfg.beta2),
+                  eps=cfg.adam_eps)
+        amp_col = raw_width(self.n) - 1
+        alpha = self.mix.params[:, amp_col]
+        alpha = torch.exp(alpha) if cfg.amp_mode == BRIGHTNESS else torch.sigmoid(alpha)
+        low = alpha < cfg.threshold() / 100.0
+        self.low_count = torch.where(low, self.low_count + 1, torch.zeros_like(self.low_count))
+        ms = (time.perf_counter() - t0) * 1e3
+        return MetricsRow(self.step_no, res.loss, int(self.live_components()), 1.0 - res.kept_fraction, ms)
+
+    def live_components(self) -> int:
+        return int(self.mix.G - int(((self.mix.flags & FLAG_FROZEN) != 0).sum()))
+
+    # -- refinement events ---------------------------------------------
+    def phase_event(self):
+        cfg, n = self.cfg, self.n
+        t = cfg.threshold()
+        mix = self.mix
+        params = mix.params.double().cpu().numpy()
+        child = mix.child.double().cpu().numpy()
+        flags = mix.flags.cpu().numpy().copy()
+        G = mix.G
+        ms, cs, cols, amp = raw_slices(n)
+        has_child = (flags & FLAG_CHILD) != 0
+        frozen = (flags & FLAG_FROZEN) != 0
+        # freeze-out: activated amplitude below t/100 for the whole phase
+        newly_frozen = (self.low_count.cpu().numpy() >= cfg.phase_length) & ~frozen
+        frozen |= newly_frozen
+        # check_materialize: child's activated amplitude >= t
+        idx = np.flatnonzero(has_child & ~frozen & (_amp(child[:, amp], cfg.amp_mode) >= t))
+        # materialize: composed mean / factor, activations inverted with clamping
+        Lp = _activate(params[idx][:, cs], n)
+        U = _activate(child[idx][:, cs], n)
+        mc = np.einsum("eik,ek->ei", Lp, child[idx][:, ms]) + params[idx][:, ms]
+        Lc = Lp @ U
+        new_rows = np.zeros((idx.size, raw_width(n)))
+        new_rows[:, ms] = mc
+        new_rows[:, cs], clamped = _inverse_activate(Lc, n)
+        new_rows[:, cols] = child[idx][:, cols]
+        new_rows[:, amp] = child[idx][:, amp]
+        params = np.concatenate([params, new_rows]).astype(np.float32)
+        # spawn_children for every live component without a child: the
+        # materialised parents (their child just became a component) and the new components
+        needs = np.concatenate([~has_child | np.isin(np.arange(G), idx), np.ones(idx.size, bool)])
+        frozen = np.concatenate([frozen, np.zeros(idx.size, bool)])
+        needs &= ~frozen
+        child = np.concatenate([child, np.zeros((idx.size, raw_width(n)))]).astype(np.float32)
+        child[needs] = spawn_rows(n, int(needs.sum()), cfg.amp_mode, t, self.rng)
+        hc = np.concatenate([has_child, np.zeros(idx.size, bool)]) | needs
+        hc &= ~frozen
+        # Adam moments: old slots kept, new rows and re-spawned children start at zero
+        st = {k: v.cpu().numpy() for k, v in self.state.items()}
+        Gn = params.shape[0]
+        for key in ("m1p", "m2p"):
+            st[key] = np.concatenate([st[key], np.zeros((idx.size, raw_width(n)), np.float32)])
+        for key in ("m1c", "m2c"):
+            st[key] = np.concatenate([st[key], np.zeros((idx.size, raw_width(n)), np.float32)])
+            st[key][needs] = 0.0
+        self.mix = Mixture.from_arrays(n, cfg.amp_mode, params, child, hc, frozen, device=self.device)
+        self.state = {k: torch.from_numpy(np.ascontiguousarray(v)).to(self.device) for k, v in st.items()}
+        self.low_count = torch.zeros(Gn, dtype=torch.int32, device=self.device)
+        self.last_good = self.mix.clone()
+        return dict(iteration=self.step_no, materialized=int(idx.size), spawned=int(needs.sum()),
+                    frozen=int(newly_frozen.sum()), clamped=int(clamped), n_components=Gn)
+
+
+def train(cfg: TrainConfig, target, n_dims: int, *, mixture: Mixture | None = None, device=None, allreduce=None,
+          rank: int = 0, world: int = 1, callback=None) -> TrainResult:
+    """SPEC.md:326-334. Returns the final mixture, one MetricsRow per iteration and the refinement
+    events. 0 iterations returns the initial mixture unchanged."""
+    tr = Trainer(cfg, target, n_dims, mixture=mixture, device=device, allreduce=allreduce, rank=rank, world=world)
+    out = TrainResult(tr.mix)
+    for it in range(cfg.iterations):
+        row = tr.iteration()
+        out.metrics.append(row)
+        if callback:
+            callback(tr, row)
+        if (it + 1) % cfg.phase_length == 0 and (it + 1) // cfg.phase_length >= cfg.warmup_phases:
+            out.events.append(tr.phase_event())
+    out.mixture = tr.mix
+    return out
+
+
+def held_out_rel_l2(mix: Mixture, target, n_dims: int, n: int = 1 << 14, seed: int = 12345, tile_size: int = 256):
+    """Relative L2 of the mixture against the target on fresh held-out queries."""
+    g = torch.Generator(device=mix.device)
+    g.manual_seed(seed)
+    q, tg = D.sample_batch(target, n_dims, n, tile_size, g, mix.device)
+    hp = HotPath(n_dims, tile_size=tile_size, device=mix.device)
+    pred = hp.evaluate(mix, q, cull=True)
+    return float(torch.linalg.norm(pred - tg) / torch.linalg.norm(tg))
