@@ -184,55 +184,71 @@ class Trainer:
 
     # -- refinement events ---------------------------------------------
     def phase_event(self):
+        """One refinement boundary: freeze-out, check_materialize + materialize, spawn_children."""
+        ev = self.materialize_step()
+        ev["spawned"] = self.spawn_step()
+        ev["n_components"] = self.mix.G
+        self.last_good = self.mix.clone()
+        return ev
+
+    def _host(self):
+        mix = self.mix
+        return (mix.params.double().cpu().numpy(), mix.child.double().cpu().numpy(), mix.flags.cpu().numpy().copy(),
+                {k: v.cpu().numpy() for k, v in self.state.items()})
+
+    def _upload(self, params, child, has_child, frozen, st):
+        self.mix = Mixture.from_arrays(self.n, self.cfg.amp_mode, params.astype(np.float32), child.astype(np.float32),
+                                       has_child, frozen, device=self.device)
+        self.state = {k: torch.from_numpy(np.ascontiguousarray(v)).to(self.device) for k, v in st.items()}
+        if self.low_count.shape[0] != self.mix.G:
+            self.low_count = torch.cat([self.low_count, torch.zeros(self.mix.G - self.low_count.shape[0],
+                                                                    dtype=torch.int32, device=self.device)])
+
+    def materialize_step(self):
+        """Freeze-out, then check_materialize and materialize
+        (SPEC.md:356-364): each selected child becomes a standalone component (composed mean and
+        factor, activations inverted with off-diagonal clamping); its parent loses the child."""
         cfg, n = self.cfg, self.n
         t = cfg.threshold()
-        mix = self.mix
-        params = mix.params.double().cpu().numpy()
-        child = mix.child.double().cpu().numpy()
-        flags = mix.flags.cpu().numpy().copy()
-        G = mix.G
+        params, child, flags, st = self._host()
         ms, cs, cols, amp = raw_slices(n)
         has_child = (flags & FLAG_CHILD) != 0
         frozen = (flags & FLAG_FROZEN) != 0
-        # freeze-out: activated amplitude below t/100 for the whole phase
         newly_frozen = (self.low_count.cpu().numpy() >= cfg.phase_length) & ~frozen
         frozen |= newly_frozen
-        # check_materialize: child's activated amplitude >= t
-        idx = np.flatnonzero(has_child & ~frozen & (_amp(child[:, amp], cfg.amp_mode) >= t))
-        # materialize: composed mean / factor, activations inverted with clamping
+        has_child &= ~frozen
+        idx = np.flatnonzero(has_child & (_amp(child[:, amp], cfg.amp_mode) >= t))
         Lp = _activate(params[idx][:, cs], n)
         U = _activate(child[idx][:, cs], n)
         mc = np.einsum("eik,ek->ei", Lp, child[idx][:, ms]) + params[idx][:, ms]
-        Lc = Lp @ U
         new_rows = np.zeros((idx.size, raw_width(n)))
         new_rows[:, ms] = mc
-        new_rows[:, cs], clamped = _inverse_activate(Lc, n)
+        new_rows[:, cs], clamped = _inverse_activate(Lp @ U, n)
         new_rows[:, cols] = child[idx][:, cols]
         new_rows[:, amp] = child[idx][:, amp]
-        params = np.concatenate([params, new_rows]).astype(np.float32)
-        # spawn_children for every live component without a child: the
-        # materialised parents (their child just became a component) and the new components
-        needs = np.concatenate([~has_child | np.isin(np.arange(G), idx), np.ones(idx.size, bool)])
-        frozen = np.concatenate([frozen, np.zeros(idx.size, bool)])
-        needs &= ~frozen
-        child = np.concatenate([child, np.zeros((idx.size, raw_width(n)))]).astype(np.float32)
-        child[needs] = spawn_rows(n, int(needs.sum()), cfg.amp_mode, t, self.rng)
-        hc = np.concatenate([has_child, np.zeros(idx.size, bool)]) | needs
-        hc &= ~frozen
-        # Adam moments: old slots kept, new rows and re-spawned children start at zero
-        st = {k: v.cpu().numpy() for k, v in self.state.items()}
-        Gn = params.shape[0]
-        for key in ("m1p", "m2p"):
-            st[key] = np.concatenate([st[key], np.zeros((idx.size, raw_width(n)), np.float32)])
+        has_child[idx] = False
+        k = idx.size
+        zeros = np.zeros((k, raw_width(n)))
+        for key in st:                                  # new slots start with zero moments (SPEC.md:322)
+            st[key] = np.concatenate([st[key], zeros.astype(np.float32)])
+        self._upload(np.concatenate([params, new_rows]), np.concatenate([child, zeros]),
+                     np.concatenate([has_child, np.zeros(k, bool)]), np.concatenate([frozen, np.zeros(k, bool)]), st)
+        self.low_count.zero_()
+        return dict(iteration=self.step_no, materialized=int(k), frozen=int(newly_frozen.sum()), clamped=int(clamped))
+
+    def spawn_step(self) -> int:
+        """spawn_children: every live component without a child gets one (U = I,
+        m_u = 0, colour in +-0.1 raw, activated amplitude t/10) with zeroed moments."""
+        cfg, n = self.cfg, self.n
+        params, child, flags, st = self._host()
+        has_child = (flags & FLAG_CHILD) != 0
+        frozen = (flags & FLAG_FROZEN) != 0
+        needs = ~has_child & ~frozen
+        child[needs] = spawn_rows(n, int(needs.sum()), cfg.amp_mode, cfg.threshold(), self.rng)
         for key in ("m1c", "m2c"):
-            st[key] = np.concatenate([st[key], np.zeros((idx.size, raw_width(n)), np.float32)])
             st[key][needs] = 0.0
-        self.mix = Mixture.from_arrays(n, cfg.amp_mode, params, child, hc, frozen, device=self.device)
-        self.state = {k: torch.from_numpy(np.ascontiguousarray(v)).to(self.device) for k, v in st.items()}
-        self.low_count = torch.zeros(Gn, dtype=torch.int32, device=self.device)
-        self.last_good = self.mix.clone()
-        return dict(iteration=self.step_no, materialized=int(idx.size), spawned=int(needs.sum()),
-                    frozen=int(newly_frozen.sum()), clamped=int(clamped), n_components=Gn)
+        self._upload(params, child, has_child | needs, frozen, st)
+        return int(needs.sum())
 
 
 def train(cfg: TrainConfig, target, n_dims: int, *, mixture: Mixture | None = None, device=None, allreduce=None,
