@@ -17,10 +17,21 @@ using namespace ndg;
 
 namespace {
 
-constexpr int kBwdThreads = kBwdChunk;
-#ifndef NDG_BWD_PIPE
-#define NDG_BWD_PIPE 0
+#ifndef NDG_BWD_FFMA2
+#define NDG_BWD_FFMA2 0
 #endif
+#ifndef NDG_BWD_UNROLL
+#define NDG_BWD_UNROLL 2
+#endif
+
+constexpr int kBwdThreads = kBwdChunk;
+constexpr int kBwdUnroll = NDG_BWD_UNROLL;
+
+__host__ __device__ constexpr int srow_start(int i) {   // sum_{r<i} (r/2 + 1): packed S row offsets
+    int s = 0;
+    for (int r = 0; r < i; ++r) s += r / 2 + 1;
+    return s;
+}
 #ifndef NDG_BWD_MINB
 #define NDG_BWD_MINB 3
 #endif
@@ -78,19 +89,21 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     mbar_wait(&bar, 0);
     if (!active) return;
 
-    float S[P], tv[N], gA[3], ls = 0.f, px = 0.f;
+#if NDG_BWD_FFMA2
+    // Packed FP32x2 (FFMA2) layout: z2[kp] = (z~_{2kp}, z~_{2kp+1}); row i of S is kept as
+    // i/2 + 1 pairs (S_i,2jp , S_i,2jp+1); the pair's second slot past the diagonal is scratch.
+    constexpr int NZP = (N + 1) / 2;
+    constexpr int NSP = srow_start(N);
+    float2 Sp[NSP], tv2[NZP];
+    float gA0 = 0.f, gA1 = 0.f, gA2 = 0.f, ls = 0.f, px = 0.f;
 #pragma unroll
-    for (int i = 0; i < P; ++i) S[i] = 0.f;
+    for (int i = 0; i < NSP; ++i) Sp[i] = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < N; ++i) tv[i] = 0.f;
-    gA[0] = gA[1] = gA[2] = 0.f;
+    for (int i = 0; i < NZP; ++i) tv2[i] = make_float2(0.f, 0.f);
 
-#if NDG_BWD_PIPE
-    // software-pipelined: z~ of query q+1 is computed while query q's outer products accumulate
-    float zn[N], sn;
-    auto solve = [&](int q, float* z, float& s2, float* dq) {
-        const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
+    for (int q = 0; q < tile; ++q) {
         float xq[QS];
+        const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
 #pragma unroll
         for (int v = 0; v < QS / 4; ++v) {
             const float4 x = q4[v];
@@ -99,47 +112,73 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
             xq[4 * v + 2] = x.z;
             xq[4 * v + 3] = x.w;
         }
-        s2 = 0.f;
+        float2 z2[NZP];
+        z2[NZP - 1] = make_float2(0.f, 0.f);            // pad slot when N is odd
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb(N) + i]);
+            float2 acc = make_float2(fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]), 0.f);
 #pragma unroll
-            for (int k = 0; k < i; ++k) acc = fmaf(r[rec_lu(N) + tri_s(i, k)], z[k], acc);
-            z[i] = acc;
-            s2 = fmaf(acc, acc, s2);
+            for (int kp = 0; kp < i / 2; ++kp)
+                acc = __ffma2_rn(make_float2(r[rec_l(N, i, 2 * kp)], r[rec_l(N, i, 2 * kp) + 1]), z2[kp], acc);
+            if (i & 1) acc.x = fmaf(r[rec_l(N, i, i - 1)], z2[(i - 1) / 2].x, acc.x);
+            const float zi = acc.x + acc.y;
+            if (i & 1) z2[i / 2].y = zi;
+            else z2[i / 2].x = zi;
         }
-        dq[0] = xq[N];
-        dq[1] = xq[N + 1];
-        dq[2] = xq[N + 2];
-        dq[3] = xq[N + 3];
-    };
-    float dqn[4];
-    solve(0, zn, sn, dqn);
-    for (int q = 0; q < tile; ++q) {
-        float z[N], dq[4];
-        const float s2 = sn;
+        float2 ss = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < N; ++i) z[i] = zn[i];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) dq[i] = dqn[i];
-        if (q + 1 < tile) solve(q + 1, zn, sn, dqn);
+        for (int kp = 0; kp < NZP; ++kp) ss = __ffma2_rn(z2[kp], z2[kp], ss);
+        const float s2 = ss.x + ss.y;
         const float g = ex2_neg(s2);
-        const float h = fmaf(dq[2], r[A0 + 2], fmaf(dq[1], r[A0 + 1], dq[0] * r[A0]));
+        const float dp0 = xq[N], dp1 = xq[N + 1], dp2 = xq[N + 2], ell = xq[N + 3];
+        const float h = fmaf(dp2, r[A0 + 2], fmaf(dp1, r[A0 + 1], dp0 * r[A0]));
         const float wgt = g * h;
+        float2 u2[NZP];
+#pragma unroll
+        for (int kp = 0; kp < NZP; ++kp) {
+            u2[kp] = __fmul2_rn(make_float2(wgt, wgt), z2[kp]);
+            tv2[kp] = __fadd2_rn(tv2[kp], u2[kp]);
+        }
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            const float u = wgt * z[i];
-            tv[i] += u;
+            const float ui = (i & 1) ? u2[i / 2].y : u2[i / 2].x;
 #pragma unroll
-            for (int j = 0; j <= i; ++j) S[tri(i, j)] = fmaf(u, z[j], S[tri(i, j)]);
+            for (int jp = 0; jp <= i / 2; ++jp)
+                Sp[srow_start(i) + jp] = __ffma2_rn(make_float2(ui, ui), z2[jp], Sp[srow_start(i) + jp]);
         }
-        gA[0] = fmaf(g, dq[0], gA[0]);
-        gA[1] = fmaf(g, dq[1], gA[1]);
-        gA[2] = fmaf(g, dq[2], gA[2]);
-        ls = fmaf(g, dq[3], ls);
+        gA0 = fmaf(g, dp0, gA0);
+        gA1 = fmaf(g, dp1, gA1);
+        gA2 = fmaf(g, dp2, gA2);
+        ls = fmaf(g, ell, ls);
         px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
     }
+
+    double* out = accum + e * A;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            const float2 v = Sp[srow_start(i) + j / 2];
+            atomicAdd(out + tri(i, j), (double)((j & 1) ? v.y : v.x));
+        }
+#pragma unroll
+    for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
+    atomicAdd(out + P + N, (double)gA0);
+    atomicAdd(out + P + N + 1, (double)gA1);
+    atomicAdd(out + P + N + 2, (double)gA2);
+    atomicAdd(out + P + N + 3, (double)ls);
+    atomicAdd(out + P + N + 4, (double)px);
+    atomicAdd(out + P + N + 5, (double)tile);
 #else
+    // scalar FP32: one FFMA per multiply-add (the packed variant adds pad work)
+    float S[P], tv[N], gA[3], ls = 0.f, px = 0.f;
+#pragma unroll
+    for (int i = 0; i < P; ++i) S[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) tv[i] = 0.f;
+    gA[0] = gA[1] = gA[2] = 0.f;
+
+#pragma unroll kBwdUnroll
     for (int q = 0; q < tile; ++q) {
         float xq[QS];
         const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
@@ -155,9 +194,9 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
         float s2 = 0.f;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb(N) + i]);
+            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]);
 #pragma unroll
-            for (int k = 0; k < i; ++k) acc = fmaf(r[rec_lu(N) + tri_s(i, k)], z[k], acc);
+            for (int k = 0; k < i; ++k) acc = fmaf(r[rec_l(N, i, k)], z[k], acc);
             z[i] = acc;
             s2 = fmaf(acc, acc, s2);
         }
@@ -179,7 +218,6 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
         px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
     }
 
-#endif
 
     double* out = accum + e * A;
 #pragma unroll
@@ -192,6 +230,7 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     atomicAdd(out + P + N + 3, (double)ls);
     atomicAdd(out + P + N + 4, (double)px);
     atomicAdd(out + P + N + 5, (double)tile);
+#endif
 }
 
 template <int N>

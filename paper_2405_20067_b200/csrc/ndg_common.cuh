@@ -22,18 +22,27 @@ __host__ __device__ constexpr int64_t imin64(int64_t a, int64_t b) { return a < 
 __host__ __device__ constexpr int raw_floats(int n) { return n + n_chol(n) + 4; }
 
 // Evaluation record (float32), one per evaluated Gaussian, 16-byte multiple so a record is one
-// cp.async.bulk and a run of LDS.128 broadcasts:
-//   rho[N]   = C / L_ii                 (C = sqrt(0.5 * log2 e): folds the -1/2 and ln->log2)
-//   nb[N]    = -C * m_i / L_ii
-//   nlu[S]   = -L_ij / L_ii, strict lower, row-major (S = N(N-1)/2)
-//   a[3]     = alpha * sigmoid(color)   (premultiplied colour)
+// cp.async.bulk and a run of LDS.128 broadcasts. Laid out for packed FP32x2 (FFMA2) use:
+//   nb2[2N]  = (nb_i, nb_i), nb_i = -C * m_i / L_ii   (duplicated: the addend operand of FFMA2 is a pair)
+//   rho[N]   = C / L_ii                                (C = sqrt(0.5 * log2 e): folds the -1/2 and ln->log2)
+//   nlu[..]  = -L_ij / L_ii, strict lower, row i padded to an even length so (j, j+1) pairs are
+//              8-byte aligned (the backward's packed row dot products); the pad entries are 0
+//   a[3]     = alpha * sigmoid(color)                  (premultiplied colour)
 // so z~_i = fma(rho_i, x_i, nb_i) + sum_j nlu_ij z~_j equals C * z_i of L z = x - m
 // and g = exp2(-|z~|^2) = exp(-|z|^2 / 2).
-__host__ __device__ constexpr int rec_rho(int) { return 0; }
-__host__ __device__ constexpr int rec_nb(int n) { return n; }
-__host__ __device__ constexpr int rec_lu(int n) { return 2 * n; }
-__host__ __device__ constexpr int rec_a(int n) { return 2 * n + n_strict(n); }
-__host__ __device__ constexpr int rec_floats(int n) { return pad4(2 * n + n_strict(n) + 3); }
+__host__ __device__ constexpr int pad2(int x) { return (x + 1) & ~1; }
+__host__ __device__ constexpr int rec_nb2(int) { return 0; }
+__host__ __device__ constexpr int rec_rho(int n) { return 2 * n; }
+__host__ __device__ constexpr int rec_lu(int n) { return pad2(3 * n); }
+__host__ __device__ constexpr int lu_row_start(int i) {   // sum_{r<i} 2*ceil(r/2)
+    int s = 0;
+    for (int r = 0; r < i; ++r) s += 2 * ((r + 1) / 2);
+    return s;
+}
+__host__ __device__ constexpr int lu_floats(int n) { return lu_row_start(n); }
+__host__ __device__ constexpr int rec_l(int n, int i, int j) { return rec_lu(n) + lu_row_start(i) + j; }
+__host__ __device__ constexpr int rec_a(int n) { return rec_lu(n) + lu_floats(n); }
+__host__ __device__ constexpr int rec_floats(int n) { return pad4(rec_a(n) + 3); }
 
 // Backward query record (float32): x[N] | dpred[3] | ell, produced by the fused forward+loss.
 __host__ __device__ constexpr int qrec_floats(int n) { return pad4(n + 4); }

@@ -16,13 +16,19 @@ using namespace ndg;
 
 namespace {
 
-constexpr int kChunk = 32;                  // candidate records per ring stage (one per lane of warp 0)
+#ifndef NDG_FWD_CHUNK
+#define NDG_FWD_CHUNK 16
+#endif
+#ifndef NDG_FWD_STAGES
+#define NDG_FWD_STAGES 4
+#endif
+constexpr int kChunk = NDG_FWD_CHUNK;       // candidate records per ring stage (one per lane of warp 0)
 
 // Launch shape per N: QPT queries per thread x NT threads = 256 queries per pass (one tile).
 #ifndef NDG_FWD_QPT
 #define NDG_FWD_QPT 4
 #endif
-template <int N> struct FwdCfg { static constexpr int QPT = NDG_FWD_QPT, NT = 256 / NDG_FWD_QPT, STAGES = 2; };
+template <int N> struct FwdCfg { static constexpr int QPT = NDG_FWD_QPT, NT = 256 / NDG_FWD_QPT, STAGES = NDG_FWD_STAGES; };
 template <> struct FwdCfg<11> { static constexpr int QPT = 2, NT = 128, STAGES = 4; };
 template <> struct FwdCfg<12> { static constexpr int QPT = 2, NT = 128, STAGES = 4; };
 template <> struct FwdCfg<13> { static constexpr int QPT = 2, NT = 128, STAGES = 4; };
@@ -77,7 +83,9 @@ __global__ void __launch_bounds__(NT)
     double loss_acc = 0.0;
     uint32_t ring = 0;   // ring position across passes (stage = ring % STAGES, parity = ring / STAGES)
     for (int q0 = 0; q0 < tile; q0 += NT * QPT) {
-        float x[QPT][N], p[QPT][3];
+        // queries j and j + QPT/2 of this thread form packed pair jp: x2[jp][d] = (x_j[d], x_{j+QPT/2}[d])
+        constexpr int NP = QPT / 2;
+        float2 x2[NP][N], p2[NP][3];
         bool valid[QPT];
 #pragma unroll
         for (int j = 0; j < QPT; ++j) {
@@ -85,9 +93,14 @@ __global__ void __launch_bounds__(NT)
             valid[j] = qi < tile;
             const float* src = queries + (t * tile + qi) * N;
 #pragma unroll
-            for (int d = 0; d < N; ++d) x[j][d] = valid[j] ? src[d] : 0.f;
-            p[j][0] = p[j][1] = p[j][2] = 0.f;
+            for (int d = 0; d < N; ++d) {
+                const float v = valid[j] ? src[d] : 0.f;
+                if (j < NP) x2[j][d].x = v;
+                else x2[j - NP][d].y = v;
+            }
         }
+#pragma unroll
+        for (int jp = 0; jp < NP; ++jp) p2[jp][0] = p2[jp][1] = p2[jp][2] = make_float2(0.f, 0.f);
         if (warp == 0) {
             for (int c = 0; c < STAGES && c < nchunks; ++c) {
                 const uint32_t pos = ring + c;
@@ -100,10 +113,9 @@ __global__ void __launch_bounds__(NT)
             const int s = (int)(pos % STAGES);
             mbar_wait(&full_bar[s], (pos / STAGES) & 1);
             const int n_in = (int)imin64(kChunk, end - beg - (int64_t)c * kChunk);
-            const float* sr = s_rec + s * kChunk * RS;
-            for (int ci = 0; ci < n_in; ++ci) {
+            const float4* r4 = reinterpret_cast<const float4*>(s_rec + s * kChunk * RS);
+            for (int ci = 0; ci < n_in; ++ci, r4 += RS / 4) {   // pointer bump: no IMAD on the FMA pipe
                 float r[RS];
-                const float4* r4 = reinterpret_cast<const float4*>(sr + ci * RS);
 #pragma unroll
                 for (int v = 0; v < RS / 4; ++v) {
                     const float4 w = r4[v];
@@ -113,21 +125,24 @@ __global__ void __launch_bounds__(NT)
                     r[4 * v + 3] = w.w;
                 }
 #pragma unroll
-                for (int j = 0; j < QPT; ++j) {
-                    float z[N];
-                    float s2 = 0.f;
+                for (int jp = 0; jp < NP; ++jp) {
+                    // two queries per FFMA2: the record coefficient is the broadcast scalar operand
+                    float2 z[N];
+                    float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int i = 0; i < N; ++i) {
-                        float acc = fmaf(r[rec_rho(N) + i], x[j][i], r[rec_nb(N) + i]);
+                        float2 acc = __ffma2_rn(make_float2(r[rec_rho(N) + i], r[rec_rho(N) + i]), x2[jp][i],
+                                                make_float2(r[rec_nb2(N) + 2 * i], r[rec_nb2(N) + 2 * i + 1]));
 #pragma unroll
-                        for (int k = 0; k < i; ++k) acc = fmaf(r[rec_lu(N) + tri_s(i, k)], z[k], acc);
+                        for (int k = 0; k < i; ++k)
+                            acc = __ffma2_rn(make_float2(r[rec_l(N, i, k)], r[rec_l(N, i, k)]), z[k], acc);
                         z[i] = acc;
-                        s2 = fmaf(acc, acc, s2);
+                        s2 = __ffma2_rn(acc, acc, s2);
                     }
-                    const float g = ex2_neg(s2);
-                    p[j][0] = fmaf(g, r[A0], p[j][0]);
-                    p[j][1] = fmaf(g, r[A0 + 1], p[j][1]);
-                    p[j][2] = fmaf(g, r[A0 + 2], p[j][2]);
+                    const float2 g = make_float2(ex2_neg(s2.x), ex2_neg(s2.y));
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch)
+                        p2[jp][ch] = __ffma2_rn(make_float2(r[A0 + ch], r[A0 + ch]), g, p2[jp][ch]);
                 }
             }
             __syncwarp();
@@ -136,6 +151,14 @@ __global__ void __launch_bounds__(NT)
                 mbar_wait(&empty_bar[s], (pos / STAGES) & 1);  // all warps done with stage s
                 issue(c + STAGES, s);
             }
+        }
+        float p[QPT][3], x[QPT][N];
+#pragma unroll
+        for (int j = 0; j < QPT; ++j) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) p[j][ch] = j < NP ? p2[j][ch].x : p2[j - NP][ch].y;
+#pragma unroll
+            for (int d = 0; d < N; ++d) x[j][d] = j < NP ? x2[j][d].x : x2[j - NP][d].y;
         }
         ring += (uint32_t)nchunks;
 

@@ -120,14 +120,16 @@ __global__ void prologue_kernel(int n, int64_t G, int64_t Gev, int amp_mode, con
     }
     double ampr = (double)arow[n + P + 3];
     double alpha = amp_mode == NDG_BRIGHTNESS ? exp(ampr) : sigmoid64(ampr);
+    for (int t = 0; t < RS; ++t) out[t] = 0.f;   // also zeroes the row pads of nlu
     for (int r = 0; r < n; ++r) {
         double inv = 1.0 / L[tri(r, r)];
+        const float nb = (float)(-kC * m[r] * inv);
+        out[rec_nb2(n) + 2 * r] = nb;
+        out[rec_nb2(n) + 2 * r + 1] = nb;
         out[rec_rho(n) + r] = (float)(kC * inv);
-        out[rec_nb(n) + r] = (float)(-kC * m[r] * inv);
-        for (int c = 0; c < r; ++c) out[rec_lu(n) + tri_s(r, c)] = (float)(-L[tri(r, c)] * inv);
+        for (int c = 0; c < r; ++c) out[rec_l(n, r, c)] = (float)(-L[tri(r, c)] * inv);
     }
     for (int ch = 0; ch < 3; ++ch) out[rec_a(n) + ch] = (float)(alpha * sigmoid64((double)arow[n + P + ch]));
-    for (int t = rec_a(n) + 3; t < RS; ++t) out[t] = 0.f;
 }
 
 extern "C" int ndg_prologue(int n, int64_t G, int64_t Gev, int amp_mode, const float* params, const float* child,
