@@ -117,6 +117,17 @@ int ndg_forward(int n, int64_t B, int tile, const float* queries, const float* t
                 const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total, float* pred, float* qrec,
                 double* loss_partial, void* stream);
 
+/* Tensor-core records (float32 [Gev][N*pad8(N+1) + 4]): Ahat_e = [C L^-1 | C L^-1 (1/2 - m)] from K1's
+ * float64 factor (the B operand of the tcgen05 z-GEMM), followed by the colour a[3] and a pad. */
+int ndg_tc_records(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
+                   const float* rec, float* rec_tc, void* stream);
+
+/* K5+K6 on the tensor cores (tcgen05 kind::tf32, 3xTF32): same contract as ndg_forward, plus the
+ * rec_tc records; tile must be <= 256. */
+int ndg_forward_tc(int n, int64_t B, int tile, const float* queries, const float* targets,
+                   const float* rec_tc, const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total,
+                   float* pred, float* qrec, double* loss_partial, void* stream);
+
 /* Deterministic fixed-order sum of the per-tile loss partials. */
 int ndg_loss_finalize(int64_t T, const double* loss_partial, double* loss, void* stream);
 

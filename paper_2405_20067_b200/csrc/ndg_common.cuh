@@ -44,6 +44,12 @@ __host__ __device__ constexpr int rec_l(int n, int i, int j) { return rec_lu(n) 
 __host__ __device__ constexpr int rec_a(int n) { return rec_lu(n) + lu_floats(n); }
 __host__ __device__ constexpr int rec_floats(int n) { return pad4(rec_a(n) + 3); }
 
+// Tensor-core (tcgen05) record: N rows x tc_k(N) floats (Ahat_e, see ndg_forward_tc.cu); one MMA
+// column block of 128 holds tc_chunk(N) Gaussians.
+__host__ __device__ constexpr int tc_k(int n) { return ((n + 1 + 7) / 8) * 8; }
+__host__ __device__ constexpr int tc_chunk(int n) { return 128 / n < 32 ? 128 / n : 32; }   // <= one per producer lane
+__host__ __device__ constexpr int tc_rec_floats(int n) { return n * tc_k(n) + 4; }   // rows | a[3] | pad
+
 // Backward query record (float32): x[N] | dpred[3] | ell, produced by the fused forward+loss.
 __host__ __device__ constexpr int qrec_floats(int n) { return pad4(n + 4); }
 

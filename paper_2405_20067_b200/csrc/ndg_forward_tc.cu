@@ -1,0 +1,401 @@
+// K5+K6 fused forward + loss on the 5th-gen tensor cores (tcgen05, kind::tf32, 3xTF32).
+//
+// Replaces eval_mixture over each tile's candidate list (Eq. 8) + loss_rel_l2
+// (SPEC.md:253-261). The Mahalanobis solve becomes a GEMM: with the per-Gaussian record
+// Ahat_e = [C L_e^-1 | C L_e^-1 (1/2 - m_e)] (K1 + ndg_tc_records, float64 -> float32) and the
+// query features xhat_q = [x_q - 1/2, 1],
+//     z~[q, (e,i)] = sum_k xhat_q[k] Ahat_e[i][k]      (= C * z_i of L z = x - m)
+// computed by tcgen05.mma (M = 128 queries, N = 128 columns = floor(128/N) Gaussians x N rows,
+// K = pad8(N+1)) in 3xTF32 (hi*hi + hi*lo + lo*hi, fp32 accumulate in TMEM): tools/
+// tc_precision_study.py shows <= 4.4e-5 block-relative error on pred at sigma 0.02 (bar 1e-4).
+// The epilogue warps read z~ rows from TMEM and finish on the FP32 pipe:
+//     s~ = sum_i z~_i^2 (FFMA2 over column pairs),  g = ex2(-s~),  pred += g * a.
+//
+// Pipeline (384 threads): TMA bulk copies of whole candidate records into a staging ring, splitter
+// warps convert them to the hi/lo K-major B planes, one lane issues the MMAs, eight epilogue warps
+// drain TMEM (accumulators double-buffered: 2 x 2 halves x 128 columns = 512).
+#include "ndg_tc.cuh"
+
+using namespace ndg;
+
+namespace {
+
+#ifndef NDG_TC_SPLITTERS
+#define NDG_TC_SPLITTERS 2
+#endif
+#ifndef NDG_TC_STAGING
+#define NDG_TC_STAGING 8
+#endif
+constexpr int kSplit = NDG_TC_SPLITTERS;   // splitter warps (2 .. 2 + kSplit - 1)
+constexpr int kEpi0 = 2 + kSplit;           // first epilogue warp
+constexpr int kTcWarps = kEpi0 + 8;
+constexpr int kTcThreads = kTcWarps * 32;
+constexpr int kTcStages = 4;         // B-operand / colour ring
+constexpr int kTcStaging = NDG_TC_STAGING;   // raw-record staging ring depth (capped per N by the smem budget)
+constexpr int kPlane = 128 * 16;     // bytes per operand plane (128 rows x 16 B)
+#ifndef NDG_TC_TBUF
+#define NDG_TC_TBUF 2
+#endif
+constexpr int kTBuf = NDG_TC_TBUF;            // TMEM accumulator buffers (x 2 query halves)
+constexpr int kNCol = 256 / kTBuf;            // MMA N: columns per buffer and half (128 or 64)
+constexpr int kARing = 8;                     // colour ring depth (independent of the B ring)
+
+template <int N>
+struct TcCfg {
+    static constexpr int K = tc_k(N);
+    static constexpr int P = K / 4;
+    static constexpr int KS = K / 8;
+    static constexpr int C = (kNCol / N < 32 ? kNCol / N : 32);
+    static constexpr int RT = tc_rec_floats(N);       // floats per raw record (rows | a | pad)
+    static constexpr size_t kFixed = (size_t)(2 * 2 + kTcStages * 2) * P * kPlane + (size_t)kARing * C * 16;
+    static constexpr size_t kSlot = (size_t)C * RT * 4;
+    static constexpr size_t kBudget = 225 * 1024;
+    // staging depth: as deep as NDG_TC_STAGING, but the whole ring set must fit in shared memory
+    static constexpr int STG = (kFixed + kTcStaging * kSlot <= kBudget) ? kTcStaging : (int)((kBudget - kFixed) / kSlot);
+    static_assert(STG >= 2, "shared-memory budget too small for the staging ring");
+};
+
+template <int N>
+constexpr size_t tc_smem_bytes() {
+    using C_ = TcCfg<N>;
+    return C_::kFixed + (size_t)C_::STG * C_::kSlot;
+}
+
+// Warp roles: 0 = TMA producer (one cp.async.bulk per candidate record into the staging ring),
+// 1 = TMEM allocator + MMA issuer, 2..kEpi0-1 = splitters (staging -> hi/lo K-major B planes + colours),
+// kEpi0.. = epilogue (warp w: query half (w-kEpi0)/4, TMEM lane quarter w%4).
+template <int N>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    forward_tc_kernel(int tile, const float* __restrict__ queries, const float* __restrict__ targets,
+                      const float* __restrict__ rec_tc, const int64_t* __restrict__ offsets,
+                      const int32_t* __restrict__ idx, float eps, double inv3n, float* __restrict__ pred,
+                      float* __restrict__ qrec, double* __restrict__ loss_partial) {
+    using Cfg = TcCfg<N>;
+    constexpr int K = Cfg::K, P = Cfg::P, KS = Cfg::KS, C = Cfg::C, RT = Cfg::RT, STG = Cfg::STG;
+    constexpr int QS = qrec_floats(N);
+    constexpr uint32_t IDESC = tc::idesc_tf32(128, kNCol);
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sA = smem;                                        // [2 halves][hi,lo][P][128][16 B]
+    uint8_t* sB = sA + 2 * 2 * P * kPlane;                     // [stages][hi,lo][P][128][16 B]
+    float* sStage = reinterpret_cast<float*>(sB + kTcStages * 2 * P * kPlane);    // [staging][C][RT]
+    float* sAval = sStage + STG * C * RT;                                   // [kARing][C][4]
+    __shared__ __align__(8) uint64_t sfull[STG], sempty[STG];
+    __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], aempty_bar[kARing];
+    __shared__ __align__(8) uint64_t tfull_bar[kTBuf], tempty_bar[kTBuf];
+    __shared__ uint32_t s_tbase;
+    __shared__ double s_loss[8];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t t = blockIdx.x;
+    const int64_t beg = offsets[t], end = offsets[t + 1];
+    const int nchunks = (int)((end - beg + C - 1) / C);
+
+    if (tid == 0) {
+        for (int s = 0; s < STG; ++s) {
+            mbar_init(&sfull[s], 1);
+            mbar_init(&sempty[s], kSplit);
+        }
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full_bar[s], kSplit);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int s = 0; s < kARing; ++s) mbar_init(&aempty_bar[s], 8);
+        for (int b = 0; b < kTBuf; ++b) {
+            mbar_init(&tfull_bar[b], 1);
+            mbar_init(&tempty_bar[b], 8);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tc::alloc(&s_tbase, 512);
+    if (tid < 256) {   // A operand: query row tid, xhat = [x - 1/2 | 1 | 0 ...] split into hi/lo planes
+        const int h = tid >> 7, r = tid & 127;
+        float xv[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) xv[k] = 0.f;
+        if (tid < tile) {
+#pragma unroll
+            for (int d = 0; d < N; ++d) xv[d] = queries[(t * tile + tid) * N + d] - 0.5f;
+            xv[N] = 1.f;
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            float4 hi, lo;
+            tc::split_tf32(xv[4 * p], hi.x, lo.x);
+            tc::split_tf32(xv[4 * p + 1], hi.y, lo.y);
+            tc::split_tf32(xv[4 * p + 2], hi.z, lo.z);
+            tc::split_tf32(xv[4 * p + 3], hi.w, lo.w);
+            *reinterpret_cast<float4*>(sA + ((h * 2 + 0) * P + p) * kPlane + r * 16) = hi;
+            *reinterpret_cast<float4*>(sA + ((h * 2 + 1) * P + p) * kPlane + r * 16) = lo;
+        }
+    }
+    fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = s_tbase;
+
+    if (warp == 0) {
+        // ------------------------------ TMA producer -------------------------------------------
+        // lane g < C owns candidate g of every chunk; its index is loaded two chunks ahead so the
+        // dependent idx -> record address load never sits on the chunk's critical path.
+        auto load_idx = [&](int c) -> int64_t {
+            const int64_t pos = beg + (int64_t)c * C + lane;
+            return (lane < C && c < nchunks && pos < end) ? (int64_t)__ldg(idx + pos) : 0;
+        };
+        int64_t e0 = load_idx(0), e1 = load_idx(1);
+        for (int c = 0; c < nchunks; ++c) {
+            const int64_t e2 = load_idx(c + 2);
+            const int sl = c % STG;
+            if (c >= STG) mbar_wait(&sempty[sl], (uint32_t)((c / STG) - 1) & 1);
+            const int64_t cb = beg + (int64_t)c * C;
+            const int n_in = (int)imin64(C, end - cb);
+            if (lane == 0) mbar_arrive_expect_tx(&sfull[sl], (uint32_t)(n_in * RT * 4));
+            __syncwarp();
+            if (lane < n_in) bulk_g2s(sStage + (sl * C + lane) * RT, rec_tc + e0 * RT, RT * 4, &sfull[sl]);
+            e0 = e1;
+            e1 = e2;
+        }
+    } else if (warp == 1) {
+        // ------------------------------ MMA issuer ---------------------------------------------
+        if (lane == 0) {
+            const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+            for (int c = 0; c < nchunks; ++c) {
+                const int s = c % kTcStages, b = c % kTBuf;
+                mbar_wait(&full_bar[s], (uint32_t)(c / kTcStages) & 1);
+                if (c >= kTBuf) mbar_wait(&tempty_bar[b], (uint32_t)((c / kTBuf) - 1) & 1);
+                tc::fence_after();
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t d = tbase + (uint32_t)((b * 2 + h) * kNCol);
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) {
+                        const uint64_t ahi = tc::smem_desc(a_base + ((h * 2 + 0) * P + 2 * ks) * kPlane, kPlane);
+                        const uint64_t alo = tc::smem_desc(a_base + ((h * 2 + 1) * P + 2 * ks) * kPlane, kPlane);
+                        const uint64_t bhi = tc::smem_desc(b_base + ((s * 2 + 0) * P + 2 * ks) * kPlane, kPlane);
+                        const uint64_t blo = tc::smem_desc(b_base + ((s * 2 + 1) * P + 2 * ks) * kPlane, kPlane);
+                        tc::mma_tf32(d, ahi, bhi, IDESC, ks > 0 ? 1u : 0u);
+#ifndef NDG_TCX_ONEPASS
+                        tc::mma_tf32(d, ahi, blo, IDESC, 1u);
+                        tc::mma_tf32(d, alo, bhi, IDESC, 1u);
+#endif
+                    }
+                }
+                tc::commit(&empty_bar[s]);      // B stage s may be refilled
+                tc::commit(&tfull_bar[b]);      // accumulators of buffer b are ready
+            }
+        }
+        __syncwarp();
+    } else if (warp < kEpi0) {
+        // ------------------------------ splitters ----------------------------------------------
+        constexpr int NSL = kSplit * 32;
+        const int pl = (warp - 2) * 32 + lane;
+        for (int c = 0; c < nchunks; ++c) {
+            const int sl = c % STG, s = c % kTcStages;
+            const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
+            mbar_wait(&sfull[sl], (uint32_t)(c / STG) & 1);
+            const int as = c % kARing;
+            if (c >= kTcStages) mbar_wait(&empty_bar[s], (uint32_t)((c / kTcStages) - 1) & 1);
+            if (c >= kARing) mbar_wait(&aempty_bar[as], (uint32_t)((c / kARing) - 1) & 1);
+            const float* stg = sStage + sl * C * RT;
+            uint8_t* bhi = sB + (s * 2 + 0) * P * kPlane;
+            uint8_t* blo = sB + (s * 2 + 1) * P * kPlane;
+#ifndef NDG_TCX_NOSPLIT
+#pragma unroll 2
+            for (int u = pl; u < n_in * N * P; u += NSL) {       // unit = (gaussian g, row i, plane p)
+                const int g = u / (N * P), rem = u - g * (N * P);
+                const int i = rem / P, p = rem - i * P;
+                const float4 v = *reinterpret_cast<const float4*>(stg + g * RT + i * K + 4 * p);
+                float4 hi, lo;
+                tc::split_tf32(v.x, hi.x, lo.x);
+                tc::split_tf32(v.y, hi.y, lo.y);
+                tc::split_tf32(v.z, hi.z, lo.z);
+                tc::split_tf32(v.w, hi.w, lo.w);
+                const int row = g * N + i;
+                *reinterpret_cast<float4*>(bhi + p * kPlane + row * 16) = hi;
+                *reinterpret_cast<float4*>(blo + p * kPlane + row * 16) = lo;
+            }
+#endif
+            for (int u = pl; u < n_in; u += NSL)
+                *reinterpret_cast<float4*>(sAval + (as * C + u) * 4) =
+                    *reinterpret_cast<const float4*>(stg + u * RT + N * K);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&full_bar[s]);
+                mbar_arrive(&sempty[sl]);
+            }
+        }
+    } else {
+        // ------------------------------ epilogue -----------------------------------------------
+        const int h = (warp - kEpi0) >> 2, q4 = warp & 3;
+        float pp[3] = {0.f, 0.f, 0.f};
+        for (int c = 0; c < nchunks; ++c) {
+            const int as = c % kARing, b = c % kTBuf;
+            const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
+            mbar_wait(&tfull_bar[b], (uint32_t)(c / kTBuf) & 1);
+            tc::fence_after();
+            float v[kNCol];
+            const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((b * 2 + h) * kNCol);
+#pragma unroll
+            for (int j = 0; j < (C * N + 15) / 16; ++j) tc::ld16(ta + 16 * j, v + 16 * j);
+            tc::wait_ld();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[b]);      // TMEM buffer b may be overwritten
+#ifndef NDG_TCX_NOEPI
+#pragma unroll
+            for (int g = 0; g < C; ++g) {
+                if (g < n_in) {
+                    float sum;
+                    if constexpr ((N & 1) == 0) {
+                        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int i = 0; i < N; i += 2) {
+                            const float2 zz = make_float2(v[g * N + i], v[g * N + i + 1]);
+                            acc = __ffma2_rn(zz, zz, acc);
+                        }
+                        sum = acc.x + acc.y;
+                    } else {
+                        sum = 0.f;
+#pragma unroll
+                        for (int i = 0; i < N; ++i) sum = fmaf(v[g * N + i], v[g * N + i], sum);
+                    }
+                    const float gv = ex2_neg(sum);
+                    const float4 av = *reinterpret_cast<const float4*>(sAval + (as * C + g) * 4);
+                    pp[0] = fmaf(gv, av.x, pp[0]);
+                    pp[1] = fmaf(gv, av.y, pp[1]);
+                    pp[2] = fmaf(gv, av.z, pp[2]);
+                }
+            }
+#else
+            pp[0] += v[0] + v[kNCol - 1];
+#endif
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&aempty_bar[as]);
+        }
+        // tile end: pred, rel-L2 loss, backward query record of this thread's query
+        double loss_acc = 0.0;
+        const int qi = h * 128 + q4 * 32 + lane;
+        if (qi < tile) {
+            const int64_t bq = t * tile + qi;
+            pred[bq * 3] = pp[0];
+            pred[bq * 3 + 1] = pp[1];
+            pred[bq * 3 + 2] = pp[2];
+            if (targets) {
+                float* qr = qrec + bq * QS;
+                double ell = 0.0;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    const double pv = pp[ch], dv = pv - (double)targets[bq * 3 + ch], den = pv * pv + (double)eps;
+                    ell += dv * dv / den;
+                    qr[N + ch] = (float)(2.0 * dv / den * inv3n);
+                }
+                ell *= inv3n;
+#pragma unroll
+                for (int d = 0; d < N; ++d) qr[d] = queries[bq * N + d];
+                qr[N + 3] = (float)ell;
+#pragma unroll
+                for (int d = N + 4; d < QS; ++d) qr[d] = 0.f;
+                loss_acc = ell;
+            }
+        }
+        if (targets) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
+            if (lane == 0) s_loss[warp - kEpi0] = loss_acc;
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (targets && tid == 0) {
+        double sl = 0.0;
+        for (int w = 0; w < 8; ++w) sl += s_loss[w];
+        loss_partial[t] = sl;
+    }
+    if (warp == 1) {
+        tc::fence_after();
+        tc::dealloc(tbase, 512);
+    }
+}
+
+template <int N>
+int launch_forward_tc(int64_t B, int tile, const float* q, const float* tgt, const float* rec_tc, const int64_t* off,
+                      const int32_t* idx, float eps, int64_t n_total, float* pred, float* qrec, double* lp,
+                      cudaStream_t st) {
+    const int64_t T = B / tile;
+    const size_t smem = tc_smem_bytes<N>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(forward_tc_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    forward_tc_kernel<N><<<(unsigned)T, kTcThreads, smem, st>>>(tile, q, tgt, rec_tc, off, idx, eps,
+                                                                1.0 / (3.0 * (double)n_total), pred, qrec, lp);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// Ahat records for the tensor-core pair kernels: one per evaluated Gaussian, N rows x K floats,
+// row i = [C (L^-1)_i0 .. C (L^-1)_i,N-1 | C (L^-1 (1/2 - m))_i | 0 ...], computed in float64 from
+// K1's activated / composed factor (forward substitution on the identity, never forming V^-1).
+__global__ void tc_records_kernel(int n, int64_t Gev, const double* __restrict__ mean64,
+                                  const double* __restrict__ chol64, const uint8_t* __restrict__ eflags,
+                                  const float* __restrict__ rec, float* __restrict__ rec_tc) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= Gev) return;
+    const int P = n_chol(n), K = tc_k(n), RT = tc_rec_floats(n);
+    float* out = rec_tc + e * RT;
+    for (int t = 0; t < RT; ++t) out[t] = 0.f;
+    if (!(eflags[e] & 1)) return;
+    for (int ch = 0; ch < 3; ++ch) out[n * K + ch] = rec[e * rec_floats(n) + rec_a(n) + ch];   // colour a
+    double L[n_chol(NMAX)], W[n_chol(NMAX)];
+    for (int t = 0; t < P; ++t) L[t] = chol64[e * P + t];
+    for (int j = 0; j < n; ++j)                     // W = L^-1 (lower), column by column
+        for (int i = j; i < n; ++i) {
+            double acc = (i == j) ? 1.0 : 0.0;
+            for (int k = j; k < i; ++k) acc -= L[tri(i, k)] * W[tri(k, j)];
+            W[tri(i, j)] = acc / L[tri(i, i)];
+        }
+    for (int i = 0; i < n; ++i) {
+        double bias = 0.0;
+        for (int j = 0; j <= i; ++j) {
+            const double w = kC * W[tri(i, j)];
+            out[i * K + j] = (float)w;
+            bias += w * (0.5 - mean64[e * n + j]);
+        }
+        out[i * K + n] = (float)bias;
+    }
+}
+
+}  // namespace
+
+extern "C" int ndg_tc_records(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
+                              const float* rec, float* rec_tc, void* stream) {
+    if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
+    if (Gev == 0) return NDG_OK;
+    tc_records_kernel<<<(unsigned)((Gev + 127) / 128), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        n, Gev, mean64, chol64, eflags, rec, rec_tc);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+extern "C" int ndg_forward_tc(int n, int64_t B, int tile, const float* queries, const float* targets,
+                              const float* rec_tc, const int64_t* offsets, const int32_t* idx, float eps,
+                              int64_t n_total, float* pred, float* qrec, double* loss_partial, void* stream) {
+    NDG_REQUIRE(tile >= 1 && tile <= 256 && B % tile == 0, "tensor-core forward needs tile in 1..256 dividing B");
+    NDG_REQUIRE(!targets || (qrec && loss_partial && n_total > 0), "targets need qrec, loss_partial, n_total");
+    if (B == 0) return NDG_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    switch (n) {
+#define NDG_CASE(NN)                                                                                             \
+    case NN:                                                                                                     \
+        return launch_forward_tc<NN>(B, tile, queries, targets, rec_tc, offsets, idx, eps, n_total, pred, qrec, \
+                                     loss_partial, st);
+        NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
+        NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
+#undef NDG_CASE
+        default:
+            return NDG_ERR_UNSUPPORTED_DIMS;
+    }
+}

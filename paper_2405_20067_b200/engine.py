@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -81,6 +82,7 @@ class EvalRecords:
     mean64: torch.Tensor     # [Gev, N] float64
     chol64: torch.Tensor     # [Gev, P] float64 packed lower factor (composed for children)
     eflags: torch.Tensor     # [Gev] uint8: bit0 live, bit1 degenerate
+    rec_tc: torch.Tensor = None   # [Gev, N*pad8(N+1) + 4] float32 Ahat records + colour (tensor-core forward)
 
 
 @dataclass
@@ -171,7 +173,7 @@ class HotPath:
 
     def __init__(self, n_dims: int, *, k: int = 16, multiplier: float = 3.0, tile_size: int = 256,
                  eps: float = 0.01, projection_seed: int = 0, projections: ProjectionSet | None = None,
-                 device=None):
+                 device=None, forward: str | None = None):
         self.n = int(n_dims)
         self.L = K.layout(self.n)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -182,6 +184,10 @@ class HotPath:
         self.tile = int(tile_size)
         self.eps = float(eps)
         self.status = torch.zeros(4, dtype=torch.int64, device=self.device)
+        # K5 implementation: "tc" = tcgen05 z-GEMM (3xTF32), "fp32" = FP32-pipe forward substitution
+        self.forward_impl = forward or os.environ.get("NDG_FORWARD", "tc")
+        if self.forward_impl not in ("tc", "fp32"):
+            raise ValueError("forward must be 'tc' or 'fp32'")
         self.events = None   # when a dict: {"forward": [(start, end), ...], "backward": [...]} CUDA events
 
     def enable_kernel_timing(self, on: bool = True):
@@ -212,7 +218,12 @@ class HotPath:
         eflags = torch.empty(Gev, dtype=torch.uint8, device=dev)
         K.call("ndg_prologue", n, G, Gev, mix.amp_mode, _p(mix.params), _p(mix.child), _p(mix.flags), _p(rec),
                _p(mean64), _p(chol64), _p(eflags), _p(self.status), _stream())
-        return EvalRecords(Gev, rec, mean64, chol64, eflags)
+        rec_tc = None
+        if self.forward_impl == "tc":
+            kk = ((n + 1 + 7) // 8) * 8
+            rec_tc = torch.empty(Gev, n * kk + 4, dtype=torch.float32, device=dev)
+            K.call("ndg_tc_records", n, Gev, _p(mean64), _p(chol64), _p(eflags), _p(rec), _p(rec_tc), _stream())
+        return EvalRecords(Gev, rec, mean64, chol64, eflags, rec_tc)
 
     # -- K2 --------------------------------------------------------------------------------
     def project(self, recs: EvalRecords) -> ProjectedBounds:
@@ -282,8 +293,12 @@ class HotPath:
             qrec = torch.empty(B, self.L["qrec"], dtype=torch.float32, device=self.device)
             loss_part = torch.empty(T, dtype=torch.float64, device=self.device)
         self._ev("forward", 0)
-        K.call("ndg_forward", self.n, B, self.tile, _p(queries), _p(targets), _p(recs.rec), _p(cl.offsets), _p(cl.idx),
-               self.eps, int(n_total or B), _p(pred), _p(qrec), _p(loss_part), _stream())
+        if self.forward_impl == "tc":
+            K.call("ndg_forward_tc", self.n, B, self.tile, _p(queries), _p(targets), _p(recs.rec_tc),
+                   _p(cl.offsets), _p(cl.idx), self.eps, int(n_total or B), _p(pred), _p(qrec), _p(loss_part), _stream())
+        else:
+            K.call("ndg_forward", self.n, B, self.tile, _p(queries), _p(targets), _p(recs.rec), _p(cl.offsets),
+                   _p(cl.idx), self.eps, int(n_total or B), _p(pred), _p(qrec), _p(loss_part), _stream())
         self._ev("forward", 1)
         return pred, qrec, loss_part
 

@@ -41,6 +41,8 @@ SIGNATURES = {
     "ndg_backward": [_I, _L, _I, _P, _P, _P, _P, _P, _L, _P, _P],
     "ndg_epilogue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "ndg_adam": [_I, _L, _P, _P, _P, _P, _P, _I, _F, _F, _F, _F, _F, _F, _F, _P],
+    "ndg_tc_records": [_I, _L, _P, _P, _P, _P, _P, _P],
+    "ndg_forward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _F, _L, _P, _P, _P, _P],
     "ndg_fp32_probe": [_P, _I, _I, _P],
     "ndg_fp32_probe_flops": [_I, _I],
 }
@@ -79,7 +81,7 @@ class NdgLaunchError(RuntimeError):
 
 # entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
 LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_scan_counts",
-             "ndg_cull_compact", "ndg_forward", "ndg_loss_finalize", "ndg_backward", "ndg_epilogue", "ndg_adam",
+             "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_backward", "ndg_epilogue", "ndg_adam",
              "ndg_fp32_probe"}
 launch_count = 0
 

@@ -99,6 +99,7 @@ def test_projection_tilebounds_cull_bitexact(cuda, N):
     assert np.array_equal(cl.offsets.cpu().numpy(), off2) and np.array_equal(cl.idx.cpu().numpy(), idx2)
 
 
+@pytest.mark.parametrize("fwd", ["fp32", "tc"])
 @pytest.mark.parametrize("N,G,B,children,amp_mode,regime", [
     (1, 50, 512, False, 0, "R"),
     (2, 200, 1024, True, 1, "R"),
@@ -109,10 +110,10 @@ def test_projection_tilebounds_cull_bitexact(cuda, N):
     (10, 600, 2048, False, 1, "C"),
     (16, 200, 512, True, 0, "R"),
 ])
-def test_fwd_bwd_parity(cuda, N, G, B, children, amp_mode, regime):
+def test_fwd_bwd_parity(cuda, N, G, B, children, amp_mode, regime, fwd):
     ndg = _ndg()
     om, mix, q, t = _mk(N, G, B, children=children, amp_mode=amp_mode, regime=regime)
-    hp = ndg.HotPath(N, projection_seed=2)
+    hp = ndg.HotPath(N, projection_seed=2, forward=fwd)
     res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
     ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
     assert np.array_equal(res.candidates.offsets.cpu().numpy(), ref["offsets"])
@@ -127,12 +128,13 @@ def test_fwd_bwd_parity(cuda, N, G, B, children, amp_mode, regime):
         assert _rel(st[:, j], ref["stats"][:, j]) < RTOL, f"stat {j}"
 
 
-def test_cfg1_full_size_vs_c_oracle(cuda):
+@pytest.mark.parametrize("fwd", ["fp32", "tc"])
+def test_cfg1_full_size_vs_c_oracle(cuda, fwd):
     """BASELINE.json configs[0] at full size: 6-D, 4096 Gaussians, 16384 queries (64 tiles)."""
     from oracle import c_oracle as CO
     ndg = _ndg()
     om, mix, q, t = _mk(6, 4096, 16384, seed=0)
-    hp = ndg.HotPath(6, projection_seed=2)
+    hp = ndg.HotPath(6, projection_seed=2, forward=fwd)
     res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
     ref = CO.step(om, q, t, hp.ps.vectors)
     assert np.array_equal(res.candidates.offsets.cpu().numpy(), ref["offsets"])
@@ -200,3 +202,17 @@ def test_adam_matches_oracle(cuda):
     p, m1, m2 = O.adam_step(p0, g, np.zeros_like(p0), np.zeros_like(p0), 1, lr)
     p, m1, m2 = O.adam_step(p, g, m1, m2, 2, lr)
     assert np.array_equal(mix.params.cpu().numpy(), p)
+
+
+@pytest.mark.parametrize("sigma0,regime", [(0.15, "R"), (0.05, "C"), (0.02, "C")])
+def test_tc_forward_sharp_gaussians(cuda, sigma0, regime):
+    """Tensor-core forward (3xTF32 z-GEMM) vs the float64 oracle on sharp Gaussians (the regime where
+    the fp32 cancellation of the centred features is largest, tools/tc_precision_study.py)."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(10, 800, 2048, regime=regime, sigma0=sigma0)
+    hp = ndg.HotPath(10, projection_seed=2, forward="tc")
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
+    assert np.array_equal(res.candidates.idx.cpu().numpy(), ref["idx"])
+    assert _rel(res.pred.cpu().numpy(), ref["pred"]) < RTOL
+    _check_grads(10, res.grads.params.cpu().numpy(), ref["grad_parent"], "parent")

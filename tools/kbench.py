@@ -22,15 +22,15 @@ t = D.synthetic_targets(a.batch, seed=3)
 mix = ndg.Mixture.from_arrays(a.n_dims, 0, **mix_np)
 hp = ndg.HotPath(a.n_dims, projection_seed=2)
 qd, td = torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda()
-res = hp.fwd_bwd(mix, qd, td)
+res = hp.fwd_bwd(mix, qd, td, check=False)
 hp.enable_kernel_timing(True)
 for _ in range(a.iters):
-    res = hp.fwd_bwd(mix, qd, td)
+    res = hp.fwd_bwd(mix, qd, td, check=False)
 torch.cuda.synchronize()
 n = a.n_dims
 pairs = res.candidates.n_pairs_tiles * 256
 f = statistics.median(hp.kernel_ms("forward")); b = statistics.median(hp.kernel_ms("backward"))
 g = res.grads.flat.double()
-print(json.dumps(dict(lib=os.path.basename(os.environ.get("NDG_LIB", "libndg.so")), regime=a.regime, n=n,
+print(json.dumps(dict(lib=os.path.basename(os.environ.get("NDG_LIB", "libndg.so")), fwd=hp.forward_impl, regime=a.regime, n=n,
       fwd_ms=f, bwd_ms=b, fwd_tflops=pairs * (n*n+3*n+8) / f / 1e9, bwd_tflops=pairs * (2*n*n+6*n+14) / b / 1e9,
       kept=res.kept_fraction, loss=res.loss, grad_checksum=float(g.abs().sum()), pred_sum=float(res.pred.double().sum()))))
