@@ -117,7 +117,8 @@ int ndg_forward(int n, int64_t B, int tile, const float* queries, const float* t
                 const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total, float* pred, float* qrec,
                 double* loss_partial, void* stream);
 
-/* Tensor-core records (float32 [Gev][N*pad8(N+1) + 4]): Ahat_e = [C L^-1 | C L^-1 (1/2 - m)] from K1's
+/* Tensor-core records (float32 [Gev][N*pad8(N+1) + 4], rows stored plane-major [K/4][N][4]):
+ * Ahat_e = [C L^-1 | C L^-1 (1/2 - m)] from K1's
  * float64 factor (the B operand of the tcgen05 z-GEMM), followed by the colour a[3] and a pad. */
 int ndg_tc_records(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
                    const float* rec, float* rec_tc, void* stream);

@@ -112,15 +112,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    // try_wait with a suspend-time hint: the waiting warp sleeps in hardware until the phase
+    // completes (or the hint expires) instead of re-polling shared memory in a tight loop.
     uint32_t addr = smem_u32(bar);
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(addr),
-        "r"(parity)
+        "r"(parity), "r"(0x989680)
         : "memory");
 }
 

@@ -37,7 +37,7 @@ constexpr int kPlane = 128 * 16;     // bytes per operand plane (128 rows x 16 B
 #define NDG_TC_TBUF 2
 #endif
 constexpr int kTBuf = NDG_TC_TBUF;            // TMEM accumulator buffers (x 2 query halves)
-constexpr int kNCol = 256 / kTBuf;            // MMA N: columns per buffer and half (128 or 64)
+
 constexpr int kARing = 8;                     // colour ring depth (independent of the B ring)
 
 template <int N>
@@ -45,9 +45,13 @@ struct TcCfg {
     static constexpr int K = tc_k(N);
     static constexpr int P = K / 4;
     static constexpr int KS = K / 8;
-    static constexpr int C = (kNCol / N < 32 ? kNCol / N : 32);
+    // TMEM: A operand (2 halves x hi/lo x K columns) + kTBuf buffers x 2 halves x NCOL accumulator columns
+    static constexpr int ACOLS = 4 * K;
+    static constexpr int NCOL = ((512 - ACOLS) / (2 * kTBuf)) & ~15;     // MMA N (112 at N = 10)
+    static constexpr int A0 = 2 * kTBuf * NCOL;                          // first A column
+    static constexpr int C = (NCOL / N < 32 ? NCOL / N : 32);
     static constexpr int RT = tc_rec_floats(N);       // floats per raw record (rows | a | pad)
-    static constexpr size_t kFixed = (size_t)(2 * 2 + kTcStages * 2) * P * kPlane + (size_t)kARing * C * 16;
+    static constexpr size_t kFixed = (size_t)(kTcStages * 2) * P * kPlane + (size_t)kARing * C * 16;
     static constexpr size_t kSlot = (size_t)C * RT * 4;
     static constexpr size_t kBudget = 225 * 1024;
     // staging depth: as deep as NDG_TC_STAGING, but the whole ring set must fit in shared memory
@@ -72,12 +76,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                       float* __restrict__ qrec, double* __restrict__ loss_partial) {
     using Cfg = TcCfg<N>;
     constexpr int K = Cfg::K, P = Cfg::P, KS = Cfg::KS, C = Cfg::C, RT = Cfg::RT, STG = Cfg::STG;
+    constexpr int kNCol = Cfg::NCOL, kA0 = Cfg::A0;
     constexpr int QS = qrec_floats(N);
     constexpr uint32_t IDESC = tc::idesc_tf32(128, kNCol);
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sA = smem;                                        // [2 halves][hi,lo][P][128][16 B]
-    uint8_t* sB = sA + 2 * 2 * P * kPlane;                     // [stages][hi,lo][P][128][16 B]
+    uint8_t* sB = smem;                                        // [stages][hi,lo][P][128][16 B]
     float* sStage = reinterpret_cast<float*>(sB + kTcStages * 2 * P * kPlane);    // [staging][C][RT]
     float* sAval = sStage + STG * C * RT;                                   // [kARing][C][4]
     __shared__ __align__(8) uint64_t sfull[STG], sempty[STG];
@@ -108,28 +112,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         fence_mbar_init();
     }
     if (warp == 1) tc::alloc(&s_tbase, 512);
-    if (tid < 256) {   // A operand: query row tid, xhat = [x - 1/2 | 1 | 0 ...] split into hi/lo planes
-        const int h = tid >> 7, r = tid & 127;
-        float xv[K];
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp >= kEpi0) {
+        // A operand into TMEM: epilogue warp (half h, lane quarter q4) writes its 32 query rows,
+        // xhat = [x - 1/2 | 1 | 0 ...] split hi / lo, at columns [kA0 + 2hK, +K) and [kA0 + 2hK + K, +K)
+        const int h = (warp - kEpi0) >> 2, q4 = warp & 3;
+        const int qi = h * 128 + q4 * 32 + lane;
+        float hi[32], lo[32];
 #pragma unroll
-        for (int k = 0; k < K; ++k) xv[k] = 0.f;
-        if (tid < tile) {
+        for (int k = 0; k < 32; ++k) hi[k] = lo[k] = 0.f;
+        if (qi < tile) {
 #pragma unroll
-            for (int d = 0; d < N; ++d) xv[d] = queries[(t * tile + tid) * N + d] - 0.5f;
-            xv[N] = 1.f;
+            for (int d = 0; d < N; ++d) tc::split_tf32(queries[(t * tile + qi) * N + d] - 0.5f, hi[d], lo[d]);
+            hi[N] = 1.f;
         }
+        const uint32_t ta = s_tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(kA0 + h * 2 * K);
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-            float4 hi, lo;
-            tc::split_tf32(xv[4 * p], hi.x, lo.x);
-            tc::split_tf32(xv[4 * p + 1], hi.y, lo.y);
-            tc::split_tf32(xv[4 * p + 2], hi.z, lo.z);
-            tc::split_tf32(xv[4 * p + 3], hi.w, lo.w);
-            *reinterpret_cast<float4*>(sA + ((h * 2 + 0) * P + p) * kPlane + r * 16) = hi;
-            *reinterpret_cast<float4*>(sA + ((h * 2 + 1) * P + p) * kPlane + r * 16) = lo;
+        for (int k0 = 0; k0 < K; k0 += 8) {      // K is a multiple of 8; st16 writes 16, so go by 8s
+            tc::st8(ta + k0, hi + k0);
+            tc::st8(ta + K + k0, lo + k0);
         }
+        tc::wait_st();
     }
-    fence_proxy_async();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     } else if (warp == 1) {
         // ------------------------------ MMA issuer ---------------------------------------------
         if (lane == 0) {
-            const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+            const uint32_t b_base = smem_u32(sB);
             for (int c = 0; c < nchunks; ++c) {
                 const int s = c % kTcStages, b = c % kTBuf;
                 mbar_wait(&full_bar[s], (uint32_t)(c / kTcStages) & 1);
@@ -168,16 +174,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t d = tbase + (uint32_t)((b * 2 + h) * kNCol);
+                    const uint32_t ahi = tbase + (uint32_t)(kA0 + h * 2 * K), alo = ahi + K;
 #pragma unroll
                     for (int ks = 0; ks < KS; ++ks) {
-                        const uint64_t ahi = tc::smem_desc(a_base + ((h * 2 + 0) * P + 2 * ks) * kPlane, kPlane);
-                        const uint64_t alo = tc::smem_desc(a_base + ((h * 2 + 1) * P + 2 * ks) * kPlane, kPlane);
                         const uint64_t bhi = tc::smem_desc(b_base + ((s * 2 + 0) * P + 2 * ks) * kPlane, kPlane);
                         const uint64_t blo = tc::smem_desc(b_base + ((s * 2 + 1) * P + 2 * ks) * kPlane, kPlane);
-                        tc::mma_tf32(d, ahi, bhi, IDESC, ks > 0 ? 1u : 0u);
+                        tc::mma_tf32_ta(d, ahi + 8 * ks, bhi, IDESC, ks > 0 ? 1u : 0u);
 #ifndef NDG_TCX_ONEPASS
-                        tc::mma_tf32(d, ahi, blo, IDESC, 1u);
-                        tc::mma_tf32(d, alo, bhi, IDESC, 1u);
+                        tc::mma_tf32_ta(d, ahi + 8 * ks, blo, IDESC, 1u);
+                        tc::mma_tf32_ta(d, alo + 8 * ks, bhi, IDESC, 1u);
 #endif
                     }
                 }
@@ -202,10 +207,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             uint8_t* blo = sB + (s * 2 + 1) * P * kPlane;
 #ifndef NDG_TCX_NOSPLIT
 #pragma unroll 2
-            for (int u = pl; u < n_in * N * P; u += NSL) {       // unit = (gaussian g, row i, plane p)
+            for (int u = pl; u < n_in * N * P; u += NSL) {       // unit = (gaussian g, plane p, row i)
+                // records are plane-major ([p][i][4]): consecutive lanes read consecutive 16-B staging
+                // units and write consecutive rows of one plane -> both conflict-free
                 const int g = u / (N * P), rem = u - g * (N * P);
-                const int i = rem / P, p = rem - i * P;
-                const float4 v = *reinterpret_cast<const float4*>(stg + g * RT + i * K + 4 * p);
+                const int p = rem / N, i = rem - p * N;
+                const float4 v = *reinterpret_cast<const float4*>(stg + g * RT + rem * 4);
                 float4 hi, lo;
                 tc::split_tf32(v.x, hi.x, lo.x);
                 tc::split_tf32(v.y, hi.y, lo.y);
@@ -336,7 +343,8 @@ int launch_forward_tc(int64_t B, int tile, const float* q, const float* tgt, con
     return NDG_OK;
 }
 
-// Ahat records for the tensor-core pair kernels: one per evaluated Gaussian, N rows x K floats,
+// Ahat records for the tensor-core pair kernels: one per evaluated Gaussian, N rows x K floats stored
+// plane-major ([K/4][N][4], the order the B operand's planes need), then a[3] and a pad;
 // row i = [C (L^-1)_i0 .. C (L^-1)_i,N-1 | C (L^-1 (1/2 - m))_i | 0 ...], computed in float64 from
 // K1's activated / composed factor (forward substitution on the identity, never forming V^-1).
 __global__ void tc_records_kernel(int n, int64_t Gev, const double* __restrict__ mean64,
@@ -357,14 +365,16 @@ __global__ void tc_records_kernel(int n, int64_t Gev, const double* __restrict__
             for (int k = j; k < i; ++k) acc -= L[tri(i, k)] * W[tri(k, j)];
             W[tri(i, j)] = acc / L[tri(i, i)];
         }
+    // plane-major: element (row i, column k) at ((k / 4) * n + i) * 4 + k % 4
+    auto at = [&](int i, int k) -> float& { return out[((k / 4) * n + i) * 4 + (k & 3)]; };
     for (int i = 0; i < n; ++i) {
         double bias = 0.0;
         for (int j = 0; j <= i; ++j) {
             const double w = kC * W[tri(i, j)];
-            out[i * K + j] = (float)w;
+            at(i, j) = (float)w;
             bias += w * (0.5 - mean64[e * n + j]);
         }
-        out[i * K + n] = (float)bias;
+        at(i, n) = (float)bias;
     }
 }
 
