@@ -201,6 +201,24 @@ def fp32_peak(torch, K, dev):
     return best
 
 
+def tf32_peak(torch, K, dev):
+    """Measured dense TF32 tcgen05 rate (TFLOP/s) -- the tensor roofline of the TC forward."""
+    import ctypes
+    out = torch.empty(256, device=dev)
+    s = torch.cuda.current_stream()
+    blocks, iters = 148, 20000
+    K.call("ndg_tf32_probe", ctypes.c_void_p(out.data_ptr()), blocks, iters, ctypes.c_void_p(s.cuda_stream))
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        K.call("ndg_tf32_probe", ctypes.c_void_p(out.data_ptr()), blocks, iters, ctypes.c_void_p(s.cuda_stream))
+        b.record()
+        b.synchronize()
+        best = max(best, K.load().ndg_tf32_probe_flops(blocks, iters) / (a.elapsed_time(b) * 1e-3) / 1e12)
+    return best
+
+
 def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmup, measure_e2e):
     import numpy as np
 
@@ -261,7 +279,7 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
         total_ms = float(tt)
     out = dict(total_ms=total_ms, ms_per_step=total_ms / steps, value=a.batch * world * steps / (total_ms * 1e-3),
                kept=statistics.mean(kept), pairs=statistics.mean(pairs), fwd_ms=fwd_ms, bwd_ms=bwd_ms,
-               launches=launches, clocks=clk, loss=res.loss, sigma0=s0)
+               launches=launches, clocks=clk, loss=res.loss, sigma0=s0, fwd_impl=hp.forward_impl)
 
     if measure_e2e:
         qh = torch.from_numpy(q).pin_memory()
@@ -303,6 +321,7 @@ def our_arm(a, rank, world):
     from paper_2405_20067_b200 import kernels as K
 
     peak = fp32_peak(torch, K, dev)
+    tpeak = tf32_peak(torch, K, dev)
     main, (mix_np, q, t, R) = run_regime(a, a.regime, torch, ndg, D, K, dist, rank, world, dev, a.steps, a.warmup,
                                          not a.no_e2e)
     secondary = None
@@ -329,6 +348,12 @@ def our_arm(a, rank, world):
     for v in kern.values():
         v["frac_of_measured_fp32"] = v["tflops"] / peak
         v["share_of_step"] = v["ms"] / main["ms_per_step"]
+    if main["fwd_impl"] == "tc":
+        # tensor-core forward: 3xTF32 z-GEMM, 3 * 2 * (N+1) * N algorithmic tensor flops per pair
+        tc_f = 3 * 2 * (n + 1) * n
+        t_tf = pairs * tc_f / (main["fwd_ms"] * 1e-3) / 1e12
+        kern["forward"].update(impl="tcgen05 kind::tf32 (3xTF32)", tensor_tflops=t_tf, tensor_peak_measured=tpeak,
+                               frac_of_measured_tf32=t_tf / tpeak, tensor_flops_per_pair=tc_f)
     dom = max(kern, key=lambda k: kern[k]["ms"])
     traffic = None
     try:

@@ -160,6 +160,9 @@ int ndg_adam(int n, int64_t rows, float* params, const float* grad, float* m1, f
  * `blocks` CTAs of 256 threads, each running 8 independent FFMA chains for 16 * iters steps. */
 int ndg_fp32_probe(float* out, int blocks, int iters, void* stream);
 double ndg_fp32_probe_flops(int blocks, int iters);
+/* TF32 tensor-core peak probe (tcgen05.mma kind::tf32 M=128 N=256 K=8 on resident operands). */
+int ndg_tf32_probe(float* out, int blocks, int iters, void* stream);
+double ndg_tf32_probe_flops(int blocks, int iters);
 
 #ifdef __cplusplus
 }

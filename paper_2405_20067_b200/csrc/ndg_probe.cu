@@ -4,7 +4,7 @@
 // 8 independent packed FFMA2 chains per thread (16 FMAs per step; FFMA2 reaches the FMA pipe's
 // limit with half the issue slots of scalar FFMA: 74.2 vs 72.5 TFLOP/s measured on B200), so the
 // denominator is the pipe's true peak; flops = 2 * 16 * 16 * iters per thread.
-#include "ndg_common.cuh"
+#include "ndg_tc.cuh"
 
 __global__ void __launch_bounds__(256) fp32_probe_kernel(float* out, int iters, float y, float z) {
     float2 a[8];
@@ -31,3 +31,51 @@ extern "C" int ndg_fp32_probe(float* out, int blocks, int iters, void* stream) {
 }
 
 extern "C" double ndg_fp32_probe_flops(int blocks, int iters) { return 2.0 * 16 * 16 * (double)iters * 256 * blocks; }
+
+// TF32 tensor-core peak probe (tcgen05.mma kind::tf32, M=128, N=256, K=8, operands resident in smem):
+// the roofline denominator for the tensor-core forward. One CTA per SM, one elected lane issues
+// `iters` MMAs; flops = 2 * 128 * 256 * 8 * iters per CTA.
+#include "ndg_tc.cuh"
+
+__global__ void __launch_bounds__(128) tf32_probe_kernel(int iters, float* out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < (128 + 256) * 8; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 1e-3f * (i % 7);
+    if (tid < 32) ndg::tc::alloc(&tbase, 256);
+    if (tid == 0) {
+        ndg::mbar_init(&bar, 1);
+        ndg::fence_mbar_init();
+    }
+    ndg::fence_proxy_async();
+    ndg::tc::fence_before();
+    __syncthreads();
+    ndg::tc::fence_after();
+    if (tid == 0) {
+        const uint32_t base = ndg::smem_u32(sm);
+        const uint64_t a = ndg::tc::smem_desc(base, 128 * 16);
+        const uint64_t b = ndg::tc::smem_desc(base + 128 * 8 * 4, 256 * 16);
+        for (int i = 0; i < iters; ++i) ndg::tc::mma_tf32(tbase, a, b, ndg::tc::idesc_tf32(128, 256), i > 0);
+        ndg::tc::commit(&bar);
+    }
+    ndg::mbar_wait(&bar, 0);
+    ndg::tc::fence_after();
+    float v[16];
+    ndg::tc::ld16(tbase + ((uint32_t)((tid / 32) * 32) << 16), v);
+    ndg::tc::wait_ld();
+    if (v[0] == 12345.f) out[tid] = v[1];
+    ndg::tc::fence_before();
+    __syncthreads();
+    if (tid < 32) ndg::tc::dealloc(tbase, 256);
+}
+
+extern "C" int ndg_tf32_probe(float* out, int blocks, int iters, void* stream) {
+    NDG_REQUIRE(blocks >= 1 && iters >= 1, "blocks and iters must be positive");
+    const int smem = (128 + 256) * 8 * 4;
+    tf32_probe_kernel<<<blocks, 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(iters, out);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+extern "C" double ndg_tf32_probe_flops(int blocks, int iters) { return 2.0 * 128 * 256 * 8 * (double)iters * blocks; }

@@ -45,6 +45,8 @@ SIGNATURES = {
     "ndg_forward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _F, _L, _P, _P, _P, _P],
     "ndg_fp32_probe": [_P, _I, _I, _P],
     "ndg_fp32_probe_flops": [_I, _I],
+    "ndg_tf32_probe": [_P, _I, _I, _P],
+    "ndg_tf32_probe_flops": [_I, _I],
 }
 
 ERRORS = {0: "NDG_OK", 1: "NDG_ERR_INVALID_PARAMETER", 2: "NDG_ERR_NONFINITE_GRADIENT",
@@ -70,7 +72,8 @@ def load():
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
-        fn.restype = {"ndg_last_error": C.c_char_p, "ndg_fp32_probe_flops": C.c_double}.get(name, C.c_int)
+        fn.restype = {"ndg_last_error": C.c_char_p, "ndg_fp32_probe_flops": C.c_double,
+                      "ndg_tf32_probe_flops": C.c_double}.get(name, C.c_int)
     _lib = lib
     return lib
 
@@ -82,7 +85,7 @@ class NdgLaunchError(RuntimeError):
 # entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
 LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_scan_counts",
              "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_backward", "ndg_epilogue", "ndg_adam",
-             "ndg_fp32_probe"}
+             "ndg_fp32_probe", "ndg_tf32_probe"}
 launch_count = 0
 
 
