@@ -18,10 +18,10 @@ using namespace ndg;
 namespace {
 
 #ifndef NDG_BWD_FFMA2
-#define NDG_BWD_FFMA2 0
+#define NDG_BWD_FFMA2 2
 #endif
 #ifndef NDG_BWD_UNROLL
-#define NDG_BWD_UNROLL 2
+#define NDG_BWD_UNROLL 1
 #endif
 
 constexpr int kBwdThreads = kBwdChunk;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     mbar_wait(&bar, 0);
     if (!active) return;
 
-#if NDG_BWD_FFMA2
+#if NDG_BWD_FFMA2 == 1
     // Packed FP32x2 (FFMA2) layout: z2[kp] = (z~_{2kp}, z~_{2kp+1}); row i of S is kept as
     // i/2 + 1 pairs (S_i,2jp , S_i,2jp+1); the pair's second slot past the diagonal is scratch.
     constexpr int NZP = (N + 1) / 2;
@@ -129,6 +129,81 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
 #pragma unroll
         for (int kp = 0; kp < NZP; ++kp) ss = __ffma2_rn(z2[kp], z2[kp], ss);
         const float s2 = ss.x + ss.y;
+        const float g = ex2_neg(s2);
+        const float dp0 = xq[N], dp1 = xq[N + 1], dp2 = xq[N + 2], ell = xq[N + 3];
+        const float h = fmaf(dp2, r[A0 + 2], fmaf(dp1, r[A0 + 1], dp0 * r[A0]));
+        const float wgt = g * h;
+        float2 u2[NZP];
+#pragma unroll
+        for (int kp = 0; kp < NZP; ++kp) {
+            u2[kp] = __fmul2_rn(make_float2(wgt, wgt), z2[kp]);
+            tv2[kp] = __fadd2_rn(tv2[kp], u2[kp]);
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const float ui = (i & 1) ? u2[i / 2].y : u2[i / 2].x;
+#pragma unroll
+            for (int jp = 0; jp <= i / 2; ++jp)
+                Sp[srow_start(i) + jp] = __ffma2_rn(make_float2(ui, ui), z2[jp], Sp[srow_start(i) + jp]);
+        }
+        gA0 = fmaf(g, dp0, gA0);
+        gA1 = fmaf(g, dp1, gA1);
+        gA2 = fmaf(g, dp2, gA2);
+        ls = fmaf(g, ell, ls);
+        px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
+    }
+
+    double* out = accum + e * A;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            const float2 v = Sp[srow_start(i) + j / 2];
+            atomicAdd(out + tri(i, j), (double)((j & 1) ? v.y : v.x));
+        }
+#pragma unroll
+    for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
+    atomicAdd(out + P + N, (double)gA0);
+    atomicAdd(out + P + N + 1, (double)gA1);
+    atomicAdd(out + P + N + 2, (double)gA2);
+    atomicAdd(out + P + N + 3, (double)ls);
+    atomicAdd(out + P + N + 4, (double)px);
+    atomicAdd(out + P + N + 5, (double)tile);
+#elif NDG_BWD_FFMA2 == 2
+    // scalar forward substitution (no added dependencies), packed FFMA2 for u = w z~, t += u and the
+    // outer-product rows S_i,(2jp, 2jp+1) += u_i (z~_2jp, z~_2jp+1)
+    constexpr int NZP = (N + 1) / 2;
+    constexpr int NSP = srow_start(N);
+    float2 Sp[NSP], tv2[NZP];
+    float gA0 = 0.f, gA1 = 0.f, gA2 = 0.f, ls = 0.f, px = 0.f;
+#pragma unroll
+    for (int i = 0; i < NSP; ++i) Sp[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < NZP; ++i) tv2[i] = make_float2(0.f, 0.f);
+#pragma unroll kBwdUnroll
+    for (int q = 0; q < tile; ++q) {
+        float xq[QS];
+        const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
+#pragma unroll
+        for (int v = 0; v < QS / 4; ++v) {
+            const float4 x = q4[v];
+            xq[4 * v] = x.x;
+            xq[4 * v + 1] = x.y;
+            xq[4 * v + 2] = x.z;
+            xq[4 * v + 3] = x.w;
+        }
+        float2 z2[NZP];
+        z2[NZP - 1] = make_float2(0.f, 0.f);
+        float s2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]);
+#pragma unroll
+            for (int k = 0; k < i; ++k) acc = fmaf(r[rec_l(N, i, k)], (k & 1) ? z2[k / 2].y : z2[k / 2].x, acc);
+            if (i & 1) z2[i / 2].y = acc;
+            else z2[i / 2].x = acc;
+            s2 = fmaf(acc, acc, s2);
+        }
         const float g = ex2_neg(s2);
         const float dp0 = xq[N], dp1 = xq[N + 1], dp2 = xq[N + 2], ell = xq[N + 3];
         const float h = fmaf(dp2, r[A0 + 2], fmaf(dp1, r[A0 + 1], dp0 * r[A0]));
