@@ -1,0 +1,182 @@
+"""Command-line surface of the reference, hot-path commands only:
+
+    ndgauss fit  --config PATH --out DIR [--resume CKPT]
+    ndgauss eval --ckpt PATH (--queries PATH | --grid SPEC) --out DIR [--ref PATH] [--no-cull]
+
+fit writes metrics.csv (iteration,loss,n_components,culled_fraction,ms_per_iter) and a checkpoint
+every phase and at the end; exit 0 on completion, 2 on a config error, 3 on TrainingAborted
+(SPEC.md:514-515). eval writes the predictions as an NDGT file (and PFM/PPM for a 2-D grid slice)
+and reports rel-L2 / PSNR against --ref. --grid SPEC = "d0,d1:W,H[:v]" evaluates the
+2-D slice over dims d0, d1 at W x H points with the other dims fixed at v (default 0.5).
+`gradcheck` and `bench-cull` are not provided.
+"""
+from __future__ import annotations
+
+import argparse
+import math
+import os
+import sys
+
+import numpy as np
+
+from . import formats as nio
+from .errors import ConfigError, FileFormatError, NdgError, TrainingAborted
+
+
+def _target(cfg: dict, n_dims: int, device):
+    from . import datasets as D
+    data = cfg.get("data", {})
+    kind = data.get("target", "shading")
+    if kind == "shading":
+        return D.ShadingToyTarget(int(data.get("target_seed", 0)), n_dims)
+    if kind == "gmm":
+        return D.GmmOracleTarget(int(data.get("target_seed", 0)), n_dims, int(data.get("target_components", 8)),
+                                 device=device)
+    raise ConfigError(f"unknown target {kind!r}", field="target")
+
+
+def _state_of(tr, cfg_raw):
+    m = tr.mix
+    return dict(n_dims=m.n_dims, amp_mode=m.amp_mode, iteration=tr.step_no, adam_step=tr.step_no,
+                config=cfg_raw, dataset=cfg_raw.get("data", {}),
+                rng=dict(seed=tr.cfg.seed, numpy=str(tr.rng.bit_generator.state["state"]["state"])),
+                params=m.params.cpu().numpy(), child=m.child.cpu().numpy(), flags=m.flags.cpu().numpy(),
+                m1p=tr.state["m1p"].cpu().numpy(), m2p=tr.state["m2p"].cpu().numpy(),
+                m1c=tr.state["m1c"].cpu().numpy(), m2c=tr.state["m2c"].cpu().numpy(),
+                low_count=tr.low_count.cpu().numpy())
+
+
+def cmd_fit(args) -> int:
+    import torch
+    from .gmm import FLAG_CHILD, FLAG_FROZEN, Mixture
+    from .trainer import Trainer
+    try:
+        cfg_raw = nio.parse_config(open(args.config).read())
+        cfg = nio.train_config_from(cfg_raw)
+    except ConfigError as e:
+        print(f"config error: {e}", file=sys.stderr)
+        return 2
+    n = int(cfg_raw.get("data", {}).get("n_dims", 10))
+    os.makedirs(args.out, exist_ok=True)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    target = _target(cfg_raw, n, dev)
+    mix = None
+    st = None
+    if args.resume:
+        st = nio.load_checkpoint(args.resume)
+        fl = st["flags"]
+        mix = Mixture.from_arrays(st["n_dims"], st["amp_mode"], st["params"], st["child"], (fl & FLAG_CHILD) != 0,
+                                  (fl & FLAG_FROZEN) != 0, device=dev)
+    tr = Trainer(cfg, target, n, mixture=mix, device=dev)
+    if st is not None:
+        tr.step_no = int(st["iteration"])
+        for k in ("m1p", "m2p", "m1c", "m2c"):
+            tr.state[k] = torch.from_numpy(st[k]).to(dev)
+        tr.low_count = torch.from_numpy(st["low_count"]).to(dev)
+    metrics = open(os.path.join(args.out, "metrics.csv"), "w")
+    metrics.write("iteration,loss,n_components,culled_fraction,ms_per_iter\n")
+    ckpt = os.path.join(args.out, "checkpoint.ndgc")
+    try:
+        start = tr.step_no
+        for it in range(start, cfg.iterations):
+            row = tr.iteration()
+            metrics.write(f"{row.iteration},{row.loss:.9g},{row.n_components},{row.culled_fraction:.6f},"
+                          f"{row.ms_per_iter:.3f}\n")
+            if (it + 1) % cfg.phase_length == 0:
+                if (it + 1) // cfg.phase_length >= cfg.warmup_phases:
+                    tr.phase_event()
+                nio.save_checkpoint(ckpt, _state_of(tr, cfg_raw))
+    except TrainingAborted as e:
+        nio.save_checkpoint(ckpt, _state_of(tr, cfg_raw))
+        print(f"training aborted: {e}", file=sys.stderr)
+        return 3
+    finally:
+        metrics.close()
+    nio.save_checkpoint(ckpt, _state_of(tr, cfg_raw))
+    return 0
+
+
+def _grid_queries(spec: str, n: int):
+    parts = spec.split(":")
+    d0, d1 = (int(x) for x in parts[0].split(","))
+    w, h = (int(x) for x in parts[1].split(","))
+    fixed = float(parts[2]) if len(parts) > 2 else 0.5
+    ys, xs = np.meshgrid((np.arange(h) + 0.5) / h, (np.arange(w) + 0.5) / w, indexing="ij")
+    q = np.full((h * w, n), fixed, np.float32)
+    q[:, d0] = xs.ravel()
+    q[:, d1] = ys.ravel()
+    return q, (h, w)
+
+
+def cmd_eval(args) -> int:
+    import torch
+    from .engine import HotPath
+    from .gmm import FLAG_CHILD, FLAG_FROZEN, Mixture
+    try:
+        st = nio.load_checkpoint(args.ckpt)
+    except (OSError, FileFormatError) as e:
+        print(f"cannot read checkpoint: {e}", file=sys.stderr)
+        return 2
+    n = st["n_dims"]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    fl = st["flags"]
+    # inference mixture: children are not evaluated
+    mix = Mixture.from_arrays(n, st["amp_mode"], st["params"], st["child"], np.zeros_like(fl, bool),
+                              (fl & FLAG_FROZEN) != 0, device=dev)
+    shape = None
+    if args.grid:
+        q, shape = _grid_queries(args.grid, n)
+    else:
+        q, _, _ = nio.read_ndgt(args.queries)
+        if q.shape[1] != n:
+            print("dimension mismatch between checkpoint and queries", file=sys.stderr)
+            return 2
+    os.makedirs(args.out, exist_ok=True)
+    B = q.shape[0]
+    tile = int(st["config"].get("culling", {}).get("tile_size", 256))
+    pad = (-B) % tile
+    qq = np.concatenate([q, np.repeat(q[-1:], pad, 0)]) if (pad and B) else q
+    pred = np.zeros((0, 3), np.float32)
+    if B:
+        hp = HotPath(n, tile_size=tile, device=dev)
+        pred = hp.evaluate(mix, torch.from_numpy(np.ascontiguousarray(qq)).to(dev), cull=not args.no_cull)
+        pred = pred.cpu().numpy()[:B]
+    nio.write_ndgt(os.path.join(args.out, "pred.ndgt"), q, pred)
+    if shape is not None:
+        img = pred.reshape(shape[0], shape[1], 3)
+        nio.write_pfm(os.path.join(args.out, "slice.pfm"), img)
+        nio.write_ppm(os.path.join(args.out, "slice.ppm"), img)
+    if args.ref and B:
+        _, ref, _ = nio.read_ndgt(args.ref)
+        err = float(np.linalg.norm(pred - ref) / max(np.linalg.norm(ref), 1e-30))
+        mse = float(np.mean((pred - ref) ** 2))
+        psnr = 10.0 * math.log10(max(float(ref.max()), 1e-30) ** 2 / max(mse, 1e-30))
+        print(f"rel_l2={err:.6g} psnr={psnr:.3f}")
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="ndgauss")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    f = sub.add_parser("fit")
+    f.add_argument("--config", required=True)
+    f.add_argument("--out", required=True)
+    f.add_argument("--resume")
+    e = sub.add_parser("eval")
+    e.add_argument("--ckpt", required=True)
+    g = e.add_mutually_exclusive_group(required=True)
+    g.add_argument("--queries")
+    g.add_argument("--grid")
+    e.add_argument("--out", required=True)
+    e.add_argument("--ref")
+    e.add_argument("--no-cull", action="store_true")
+    args = ap.parse_args(argv)
+    try:
+        return cmd_fit(args) if args.cmd == "fit" else cmd_eval(args)
+    except NdgError as err:
+        print(f"error: {err}", file=sys.stderr)
+        return 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

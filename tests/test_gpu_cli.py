@@ -1,0 +1,42 @@
+"""CLI fit / eval on the GPU: exit codes, metrics.csv, checkpoints, resume, outputs."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_fit_eval_resume(cuda, tmp_path):
+    from paper_2405_20067_b200 import cli
+    from paper_2405_20067_b200 import formats as F
+    cfgp = tmp_path / "fit.cfg"
+    cfgp.write_text("[trainer]\niterations = 40\nphase_length = 20\nbatch_size = 2048\nn_components = 64\n"
+                    "[data]\ntarget = gmm\nn_dims = 4\ntarget_components = 4\n")
+    out = tmp_path / "run"
+    assert cli.main(["fit", "--config", str(cfgp), "--out", str(out)]) == 0
+    rows = (out / "metrics.csv").read_text().strip().splitlines()
+    assert rows[0] == "iteration,loss,n_components,culled_fraction,ms_per_iter" and len(rows) == 41
+    ck = F.load_checkpoint(out / "checkpoint.ndgc")
+    assert ck["iteration"] == 40 and ck["params"].shape[0] >= 64
+    # resume for 20 more iterations
+    cfgp.write_text(cfgp.read_text().replace("iterations = 40", "iterations = 60"))
+    out2 = tmp_path / "run2"
+    assert cli.main(["fit", "--config", str(cfgp), "--out", str(out2), "--resume", str(out / "checkpoint.ndgc")]) == 0
+    assert F.load_checkpoint(out2 / "checkpoint.ndgc")["iteration"] == 60
+    # bad config -> exit 2
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("[trainer]\nnope = 1\n")
+    assert cli.main(["fit", "--config", str(bad), "--out", str(tmp_path / "x")]) == 2
+    # eval on a 2-D grid slice and on NDGT queries with a reference
+    ev = tmp_path / "ev"
+    assert cli.main(["eval", "--ckpt", str(out / "checkpoint.ndgc"), "--grid", "0,1:16,8", "--out", str(ev)]) == 0
+    assert os.path.exists(ev / "slice.pfm") and os.path.exists(ev / "slice.ppm")
+    q, p, _ = F.read_ndgt(ev / "pred.ndgt")
+    assert q.shape == (128, 4) and p.shape == (128, 3) and np.all(np.isfinite(p))
+    F.write_ndgt(tmp_path / "q.ndgt", q[:100], p[:100])
+    ev2 = tmp_path / "ev2"
+    assert cli.main(["eval", "--ckpt", str(out / "checkpoint.ndgc"), "--queries", str(tmp_path / "q.ndgt"),
+                     "--ref", str(tmp_path / "q.ndgt"), "--out", str(ev2), "--no-cull"]) == 0
+    _, p2, _ = F.read_ndgt(ev2 / "pred.ndgt")
+    assert p2.shape == (100, 3) and np.all(np.isfinite(p2))
