@@ -27,6 +27,10 @@ namespace {
 constexpr int kBwdThreads = kBwdChunk;
 constexpr int kBwdUnroll = NDG_BWD_UNROLL;
 
+__host__ __device__ constexpr int rpair_start(int ip) {   // sum_{p<ip} (2p + 1): row-pair offsets
+    return ip * ip;
+}
+
 __host__ __device__ constexpr int srow_start(int i) {   // sum_{r<i} (r/2 + 1): packed S row offsets
     int s = 0;
     for (int r = 0; r < i; ++r) s += r / 2 + 1;
@@ -235,6 +239,88 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
         for (int j = 0; j <= i; ++j) {
             const float2 v = Sp[srow_start(i) + j / 2];
             atomicAdd(out + tri(i, j), (double)((j & 1) ? v.y : v.x));
+        }
+#pragma unroll
+    for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
+    atomicAdd(out + P + N, (double)gA0);
+    atomicAdd(out + P + N + 1, (double)gA1);
+    atomicAdd(out + P + N + 2, (double)gA2);
+    atomicAdd(out + P + N + 3, (double)ls);
+    atomicAdd(out + P + N + 4, (double)px);
+    atomicAdd(out + P + N + 5, (double)tile);
+#elif NDG_BWD_FFMA2 == 3
+    // scalar forward substitution (no added dependencies); packed FFMA2 for u = w z~, t += u and the
+    // outer product by ROW pairs: (S_i,j , S_i+1,j) += z~_j * (u_i, u_i+1) for even i, j <= i, plus the
+    // diagonal S_i+1,i+1 -- exactly the lower triangle, no scratch slots.
+    constexpr int NZP = (N + 1) / 2;
+    constexpr int NSP = rpair_start(NZP);
+    float2 Sp[NSP], tv2[NZP];
+    float Sd[NZP];
+#pragma unroll
+    for (int i = 0; i < NZP; ++i) Sd[i] = 0.f;
+    float gA0 = 0.f, gA1 = 0.f, gA2 = 0.f, ls = 0.f, px = 0.f;
+#pragma unroll
+    for (int i = 0; i < NSP; ++i) Sp[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < NZP; ++i) tv2[i] = make_float2(0.f, 0.f);
+#pragma unroll kBwdUnroll
+    for (int q = 0; q < tile; ++q) {
+        float xq[QS];
+        const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
+#pragma unroll
+        for (int v = 0; v < QS / 4; ++v) {
+            const float4 x = q4[v];
+            xq[4 * v] = x.x;
+            xq[4 * v + 1] = x.y;
+            xq[4 * v + 2] = x.z;
+            xq[4 * v + 3] = x.w;
+        }
+        float2 z2[NZP];
+        z2[NZP - 1] = make_float2(0.f, 0.f);
+        float s2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]);
+#pragma unroll
+            for (int k = 0; k < i; ++k) acc = fmaf(r[rec_l(N, i, k)], (k & 1) ? z2[k / 2].y : z2[k / 2].x, acc);
+            if (i & 1) z2[i / 2].y = acc;
+            else z2[i / 2].x = acc;
+            s2 = fmaf(acc, acc, s2);
+        }
+        const float g = ex2_neg(s2);
+        const float dp0 = xq[N], dp1 = xq[N + 1], dp2 = xq[N + 2], ell = xq[N + 3];
+        const float h = fmaf(dp2, r[A0 + 2], fmaf(dp1, r[A0 + 1], dp0 * r[A0]));
+        const float wgt = g * h;
+        float2 u2[NZP];
+#pragma unroll
+        for (int kp = 0; kp < NZP; ++kp) {
+            u2[kp] = __fmul2_rn(make_float2(wgt, wgt), z2[kp]);
+            tv2[kp] = __fadd2_rn(tv2[kp], u2[kp]);
+        }
+#pragma unroll
+        for (int ip = 0; ip < NZP; ++ip) {
+#pragma unroll
+            for (int j = 0; j <= 2 * ip; ++j) {
+                const float zj = (j & 1) ? z2[j / 2].y : z2[j / 2].x;
+                Sp[rpair_start(ip) + j] = __ffma2_rn(make_float2(zj, zj), u2[ip], Sp[rpair_start(ip) + j]);
+            }
+            Sd[ip] = fmaf(u2[ip].y, z2[ip].y, Sd[ip]);
+        }
+        gA0 = fmaf(g, dp0, gA0);
+        gA1 = fmaf(g, dp1, gA1);
+        gA2 = fmaf(g, dp2, gA2);
+        ls = fmaf(g, ell, ls);
+        px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
+    }
+
+    double* out = accum + e * A;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            const int ip = i / 2;
+            const float v = (i & 1) ? (j == i ? Sd[ip] : Sp[rpair_start(ip) + j].y) : Sp[rpair_start(ip) + j].x;
+            atomicAdd(out + tri(i, j), (double)v);
         }
 #pragma unroll
     for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
