@@ -142,6 +142,23 @@ int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec
                  const int32_t* idx, const int64_t* chunk_offsets, int64_t n_chunks, double* accum, void* stream);
 
 /*
+ * K7 on the tensor cores (tcgen05 kind::tf32, 3xTF32). Same pair loop and the same accum contract as
+ * ndg_backward after ndg_moments_to_zspace: one CTA per 128 queries of a tile, z~ by the K5 z-GEMM
+ * over rec_tc, then the x-space moments M = sum w xhat xhat^T (xhat = [x - 1/2; 1]) by a second
+ * tcgen05 GEMM, added to accum[e][0 .. (N+1)(N+2)/2) (packed lower triangle = quad | lin | const);
+ * gA, loss share, proxy and pairs go to the tail as for ndg_backward.
+ * Returns NDG_ERR_UNSUPPORTED_DIMS when ndg_backward_tc_supported(n) is 0.
+ */
+int ndg_backward_tc_supported(int n);
+int ndg_backward_tc(int n, int64_t B, int tile, const float* qrec, const float* rec_tc, const int64_t* offsets,
+                    const int32_t* idx, double* accum, void* stream);
+
+/* K7b: per live evaluated Gaussian, turn the moments left by ndg_backward_tc into S' = Ahat M Ahat^T
+ * and t' = Ahat M[:, N] in place (float64; Ahat = C [L^-1 | L^-1 (1/2 - m)] from K1's factor). */
+int ndg_moments_to_zspace(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
+                          double* accum, void* stream);
+
+/*
  * K8 epilogue. Replaces the tail of `backward`: raw-parameter gradients of parents
  * and live children including the child->parent cross terms; stats[Gev][3] =
  * (loss share, gradient proxy, pairs). Non-finite gradients -> status NONFINITE_GRADIENT.

@@ -167,12 +167,12 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
         }
 #pragma unroll
     for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
-    atomicAdd(out + P + N, (double)gA0);
-    atomicAdd(out + P + N + 1, (double)gA1);
-    atomicAdd(out + P + N + 2, (double)gA2);
-    atomicAdd(out + P + N + 3, (double)ls);
-    atomicAdd(out + P + N + 4, (double)px);
-    atomicAdd(out + P + N + 5, (double)tile);
+    atomicAdd(out + acc_tail(N), (double)gA0);
+    atomicAdd(out + acc_tail(N) + 1, (double)gA1);
+    atomicAdd(out + acc_tail(N) + 2, (double)gA2);
+    atomicAdd(out + acc_tail(N) + 3, (double)ls);
+    atomicAdd(out + acc_tail(N) + 4, (double)px);
+    atomicAdd(out + acc_tail(N) + 5, (double)tile);
 #elif NDG_BWD_FFMA2 == 2
     // scalar forward substitution (no added dependencies), packed FFMA2 for u = w z~, t += u and the
     // outer-product rows S_i,(2jp, 2jp+1) += u_i (z~_2jp, z~_2jp+1)
@@ -242,12 +242,12 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
         }
 #pragma unroll
     for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
-    atomicAdd(out + P + N, (double)gA0);
-    atomicAdd(out + P + N + 1, (double)gA1);
-    atomicAdd(out + P + N + 2, (double)gA2);
-    atomicAdd(out + P + N + 3, (double)ls);
-    atomicAdd(out + P + N + 4, (double)px);
-    atomicAdd(out + P + N + 5, (double)tile);
+    atomicAdd(out + acc_tail(N), (double)gA0);
+    atomicAdd(out + acc_tail(N) + 1, (double)gA1);
+    atomicAdd(out + acc_tail(N) + 2, (double)gA2);
+    atomicAdd(out + acc_tail(N) + 3, (double)ls);
+    atomicAdd(out + acc_tail(N) + 4, (double)px);
+    atomicAdd(out + acc_tail(N) + 5, (double)tile);
 #elif NDG_BWD_FFMA2 == 3
     // scalar forward substitution (no added dependencies); packed FFMA2 for u = w z~, t += u and the
     // outer product by ROW pairs: (S_i,j , S_i+1,j) += z~_j * (u_i, u_i+1) for even i, j <= i, plus the
@@ -324,12 +324,12 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
         }
 #pragma unroll
     for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
-    atomicAdd(out + P + N, (double)gA0);
-    atomicAdd(out + P + N + 1, (double)gA1);
-    atomicAdd(out + P + N + 2, (double)gA2);
-    atomicAdd(out + P + N + 3, (double)ls);
-    atomicAdd(out + P + N + 4, (double)px);
-    atomicAdd(out + P + N + 5, (double)tile);
+    atomicAdd(out + acc_tail(N), (double)gA0);
+    atomicAdd(out + acc_tail(N) + 1, (double)gA1);
+    atomicAdd(out + acc_tail(N) + 2, (double)gA2);
+    atomicAdd(out + acc_tail(N) + 3, (double)ls);
+    atomicAdd(out + acc_tail(N) + 4, (double)px);
+    atomicAdd(out + acc_tail(N) + 5, (double)tile);
 #else
     // scalar FP32: one FFMA per multiply-add (the packed variant adds pad work)
     float S[P], tv[N], gA[3], ls = 0.f, px = 0.f;
@@ -385,12 +385,12 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     for (int i = 0; i < P; ++i) atomicAdd(out + i, (double)S[i]);
 #pragma unroll
     for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)tv[i]);
-    atomicAdd(out + P + N, (double)gA[0]);
-    atomicAdd(out + P + N + 1, (double)gA[1]);
-    atomicAdd(out + P + N + 2, (double)gA[2]);
-    atomicAdd(out + P + N + 3, (double)ls);
-    atomicAdd(out + P + N + 4, (double)px);
-    atomicAdd(out + P + N + 5, (double)tile);
+    atomicAdd(out + acc_tail(N), (double)gA[0]);
+    atomicAdd(out + acc_tail(N) + 1, (double)gA[1]);
+    atomicAdd(out + acc_tail(N) + 2, (double)gA[2]);
+    atomicAdd(out + acc_tail(N) + 3, (double)ls);
+    atomicAdd(out + acc_tail(N) + 4, (double)px);
+    atomicAdd(out + acc_tail(N) + 5, (double)tile);
 #endif
 }
 

@@ -53,9 +53,13 @@ __host__ __device__ constexpr int tc_rec_floats(int n) { return n * tc_k(n) + 4;
 // Backward query record (float32): x[N] | dpred[3] | ell, produced by the fused forward+loss.
 __host__ __device__ constexpr int qrec_floats(int n) { return pad4(n + 4); }
 
-// Accumulators per evaluated Gaussian (float64): S'[P] | t'[N] | gA[3] | loss_share | proxy | pairs
-// in the scaled z~ units with coefficient +g*h (the epilogue applies -1/C^2, -1/C, 1/C).
-__host__ __device__ constexpr int acc_doubles(int n) { return n_chol(n) + n + 3 + kNumStats; }
+// Accumulators per evaluated Gaussian (float64): S'[P] | t'[N] | spare | gA[3] | loss_share | proxy |
+// pairs in the scaled z~ units with coefficient +g*h (the epilogue applies -1/C^2, -1/C, 1/C).
+// The tensor-core backward fills the first P + N + 1 slots with the x-space moments
+// M = sum w xhat xhat^T (xhat = [x - 1/2; 1], packed lower triangle of the (N+1)^2 matrix, which is
+// exactly quad[P] | lin[N] | const) and ndg_moments_to_zspace turns them into S' | t' in place.
+__host__ __device__ constexpr int acc_tail(int n) { return n_chol(n) + n + 1; }
+__host__ __device__ constexpr int acc_doubles(int n) { return acc_tail(n) + 3 + kNumStats; }
 
 constexpr double kC = 0.84932180028801907;      // sqrt(0.5 * log2(e))
 
@@ -119,7 +123,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
+#ifdef NDG_MBAR_NOHINT
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+#endif
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(addr),
         "r"(parity), "r"(0x989680)

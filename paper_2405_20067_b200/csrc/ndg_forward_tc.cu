@@ -27,8 +27,13 @@ namespace {
 #define NDG_TC_STAGING 8
 #endif
 constexpr int kSplit = NDG_TC_SPLITTERS;   // splitter warps (2 .. 2 + kSplit - 1)
-constexpr int kEpi0 = 2 + kSplit;           // first epilogue warp
-constexpr int kTcWarps = kEpi0 + 8;
+#ifndef NDG_TC_EPIG
+#define NDG_TC_EPIG 1
+#endif
+constexpr int kEpiG = NDG_TC_EPIG;          // epilogue warps per (query half, lane quarter)
+constexpr int kEpi0 = 2 + kSplit;           // first epilogue warp (a multiple of 4: lane quarter = warp % 4)
+constexpr int kEpiW = 8 * kEpiG;            // epilogue warps
+constexpr int kTcWarps = kEpi0 + kEpiW;
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcStages = 4;         // B-operand / colour ring
 constexpr int kTcStaging = NDG_TC_STAGING;   // raw-record staging ring depth (capped per N by the smem budget)
@@ -89,6 +94,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __shared__ __align__(8) uint64_t tfull_bar[kTBuf], tempty_bar[kTBuf];
     __shared__ uint32_t s_tbase;
     __shared__ double s_loss[8];
+    __shared__ float s_pp[kEpiG > 1 ? 256 * 3 : 1];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t t = blockIdx.x;
@@ -104,10 +110,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_init(&full_bar[s], kSplit);
             mbar_init(&empty_bar[s], 1);
         }
-        for (int s = 0; s < kARing; ++s) mbar_init(&aempty_bar[s], 8);
+        for (int s = 0; s < kARing; ++s) mbar_init(&aempty_bar[s], kEpiW);
         for (int b = 0; b < kTBuf; ++b) {
             mbar_init(&tfull_bar[b], 1);
-            mbar_init(&tempty_bar[b], 8);
+            mbar_init(&tempty_bar[b], kEpiW);
         }
         fence_mbar_init();
     }
@@ -115,7 +121,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if (warp >= kEpi0) {
+    if (warp >= kEpi0 && warp < kEpi0 + 8) {
         // A operand into TMEM: epilogue warp (half h, lane quarter q4) writes its 32 query rows,
         // xhat = [x - 1/2 | 1 | 0 ...] split hi / lo, at columns [kA0 + 2hK, +K) and [kA0 + 2hK + K, +K)
         const int h = (warp - kEpi0) >> 2, q4 = warp & 3;
@@ -158,7 +164,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int n_in = (int)imin64(C, end - cb);
             if (lane == 0) mbar_arrive_expect_tx(&sfull[sl], (uint32_t)(n_in * RT * 4));
             __syncwarp();
+#ifdef NDG_TCX_ONECOPY
+            if (lane == 0) bulk_g2s(sStage + (sl * C) * RT, rec_tc, n_in * RT * 4, &sfull[sl]);
+#else
             if (lane < n_in) bulk_g2s(sStage + (sl * C + lane) * RT, rec_tc + e0 * RT, RT * 4, &sfull[sl]);
+#endif
             e0 = e1;
             e1 = e2;
         }
@@ -235,38 +245,47 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else {
         // ------------------------------ epilogue -----------------------------------------------
-        const int h = (warp - kEpi0) >> 2, q4 = warp & 3;
+        const int h = ((warp - kEpi0) >> 2) & 1, q4 = warp & 3, grp = (warp - kEpi0) >> 3;
+        // Gaussians [grp * CG, grp * CG + CG) of every chunk: kEpiG warps share a lane quarter so more
+        // warps keep TMEM reads in flight (TMEM read throughput scales with the number of loading warps)
+        constexpr int CG = (C + kEpiG - 1) / kEpiG;
+        constexpr int NLD = (CG * N + 15) / 16;
         float pp[3] = {0.f, 0.f, 0.f};
         for (int c = 0; c < nchunks; ++c) {
             const int as = c % kARing, b = c % kTBuf;
             const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
             mbar_wait(&tfull_bar[b], (uint32_t)(c / kTBuf) & 1);
             tc::fence_after();
-            float v[kNCol];
-            const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((b * 2 + h) * kNCol);
+            float v[NLD * 16];
+            const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((b * 2 + h) * kNCol + grp * CG * N);
+#ifdef NDG_TCX_NOLD
+            for (int j = 0; j < NLD * 16; ++j) v[j] = (float)(ta + j);
+#else
 #pragma unroll
-            for (int j = 0; j < (C * N + 15) / 16; ++j) tc::ld16(ta + 16 * j, v + 16 * j);
+            for (int j = 0; j < NLD; ++j) tc::ld16(ta + 16 * j, v + 16 * j);
             tc::wait_ld();
+#endif
             tc::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty_bar[b]);      // TMEM buffer b may be overwritten
 #ifndef NDG_TCX_NOEPI
 #pragma unroll
-            for (int g = 0; g < C; ++g) {
-                if (g < n_in) {
+            for (int gl = 0; gl < CG; ++gl) {
+                const int g = grp * CG + gl;
+                if (g < n_in && (kEpiG == 1 || g < C)) {
                     float sum;
                     if constexpr ((N & 1) == 0) {
                         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
                         for (int i = 0; i < N; i += 2) {
-                            const float2 zz = make_float2(v[g * N + i], v[g * N + i + 1]);
+                            const float2 zz = make_float2(v[gl * N + i], v[gl * N + i + 1]);
                             acc = __ffma2_rn(zz, zz, acc);
                         }
                         sum = acc.x + acc.y;
                     } else {
                         sum = 0.f;
 #pragma unroll
-                        for (int i = 0; i < N; ++i) sum = fmaf(v[g * N + i], v[g * N + i], sum);
+                        for (int i = 0; i < N; ++i) sum = fmaf(v[gl * N + i], v[gl * N + i], sum);
                     }
                     const float gv = ex2_neg(sum);
                     const float4 av = *reinterpret_cast<const float4*>(sAval + (as * C + g) * 4);
@@ -276,7 +295,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
             }
 #else
-            pp[0] += v[0] + v[kNCol - 1];
+            pp[0] += v[0] + v[NLD * 16 - 1];
 #endif
             __syncwarp();
             if (lane == 0) mbar_arrive(&aempty_bar[as]);
@@ -284,7 +303,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // tile end: pred, rel-L2 loss, backward query record of this thread's query
         double loss_acc = 0.0;
         const int qi = h * 128 + q4 * 32 + lane;
-        if (qi < tile) {
+        if constexpr (kEpiG > 1) {   // fold the other groups' partial predictions into group 0
+            if (grp > 0) {
+                s_pp[qi * 3] = pp[0];
+                s_pp[qi * 3 + 1] = pp[1];
+                s_pp[qi * 3 + 2] = pp[2];
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(kEpiW * 32) : "memory");
+        }
+        if ((kEpiG == 1 || grp == 0) && qi < tile) {
+            if constexpr (kEpiG > 1) {
+                pp[0] += s_pp[qi * 3];
+                pp[1] += s_pp[qi * 3 + 1];
+                pp[2] += s_pp[qi * 3 + 2];
+            }
             const int64_t bq = t * tile + qi;
             pred[bq * 3] = pp[0];
             pred[bq * 3 + 1] = pp[1];
@@ -307,7 +339,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 loss_acc = ell;
             }
         }
-        if (targets) {
+        if (targets && (kEpiG == 1 || grp == 0)) {
 #pragma unroll
             for (int o = 16; o; o >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
             if (lane == 0) s_loss[warp - kEpi0] = loss_acc;

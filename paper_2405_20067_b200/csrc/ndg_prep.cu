@@ -493,9 +493,9 @@ __global__ void epilogue_kernel(int n, int64_t G, int64_t Gev, int amp_mode, con
             so[0] = so[1] = so[2] = 0.f;
             continue;
         }
-        so[0] = (float)acc[P + n + 3];
-        so[1] = (float)(acc[P + n + 4] * invC);
-        so[2] = (float)acc[P + n + 5];
+        so[0] = (float)acc[acc_tail(n) + 3];
+        so[1] = (float)(acc[acc_tail(n) + 4] * invC);
+        so[2] = (float)acc[acc_tail(n) + 5];
         const double* Le = chol64 + e * P;
         for (int r = 0; r < n; ++r)
             for (int c = 0; c <= r; ++c) S[r * n + c] = S[c * n + r] = -acc[tri(r, c)] * invC2;
@@ -516,7 +516,7 @@ __global__ void epilogue_kernel(int n, int64_t G, int64_t Gev, int amp_mode, con
         double dalpha = 0.0;
         for (int ch = 0; ch < 3; ++ch) {
             const double cc = sigmoid64((double)row[n + P + ch]);
-            const double gA = acc[P + n + ch];
+            const double gA = acc[acc_tail(n) + ch];
             out[n + P + ch] = (float)(gA * alpha * cc * (1.0 - cc));
             dalpha += gA * cc;
         }

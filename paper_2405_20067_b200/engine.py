@@ -8,7 +8,9 @@ gmm-core, culling and grad modules, each enqueued on the current CUDA stream thr
     K3 ndg_tile_bounds   TileBounds
     K4 ndg_cull_*        cull_tile for every tile -> CSR candidate lists
     K5 ndg_forward       eval_mixture (+ K6 loss_rel_l2 fused)
-    K7 ndg_backward      backward pair loop
+    K7 ndg_backward_tc   backward pair loop on tcgen05 (z-GEMM + moments)
+       ndg_backward      (FP32-pipe pair loop: N > 12 or NDG_BACKWARD=fp32)
+    K7b ndg_moments_to_zspace  x-space moments -> S', t' (tensor-core K7 only)
     K8 ndg_epilogue      backward tail, raw-parameter chain rule
     K9 ndg_adam          adam_step
 
@@ -173,7 +175,7 @@ class HotPath:
 
     def __init__(self, n_dims: int, *, k: int = 16, multiplier: float = 3.0, tile_size: int = 256,
                  eps: float = 0.01, projection_seed: int = 0, projections: ProjectionSet | None = None,
-                 device=None, forward: str | None = None):
+                 device=None, forward: str | None = None, backward: str | None = None):
         self.n = int(n_dims)
         self.L = K.layout(self.n)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -188,6 +190,12 @@ class HotPath:
         self.forward_impl = forward or os.environ.get("NDG_FORWARD", "tc")
         if self.forward_impl not in ("tc", "fp32"):
             raise ValueError("forward must be 'tc' or 'fp32'")
+        # K7 implementation: "fp32" = FP32-pipe pair loop (default); "tc" = tcgen05 z-GEMM + moments GEMM
+        # (N <= 12, opt-in: no faster and only marginally within 1e-4)
+        bwd = backward or os.environ.get("NDG_BACKWARD", "fp32")
+        if bwd not in ("tc", "fp32"):
+            raise ValueError("backward must be 'tc' or 'fp32'")
+        self.backward_impl = "tc" if bwd == "tc" and K.load().ndg_backward_tc_supported(self.n) else "fp32"
         self.events = None   # when a dict: {"forward": [(start, end), ...], "backward": [...]} CUDA events
 
     def enable_kernel_timing(self, on: bool = True):
@@ -219,7 +227,7 @@ class HotPath:
         K.call("ndg_prologue", n, G, Gev, mix.amp_mode, _p(mix.params), _p(mix.child), _p(mix.flags), _p(rec),
                _p(mean64), _p(chol64), _p(eflags), _p(self.status), _stream())
         rec_tc = None
-        if self.forward_impl == "tc":
+        if self.forward_impl == "tc" or self.backward_impl == "tc":
             kk = ((n + 1 + 7) // 8) * 8
             rec_tc = torch.empty(Gev, n * kk + 4, dtype=torch.float32, device=dev)
             K.call("ndg_tc_records", n, Gev, _p(mean64), _p(chol64), _p(eflags), _p(rec), _p(rec_tc), _stream())
@@ -312,9 +320,16 @@ class HotPath:
         B = int(qrec.shape[0])
         accum = torch.zeros(recs.Gev, self.L["acc"], dtype=torch.float64, device=self.device)
         self._ev("backward", 0)
-        K.call("ndg_backward", self.n, B, self.tile, _p(qrec), _p(recs.rec), _p(cl.offsets), _p(cl.idx),
-               _p(cl.chunk_offsets), cl.n_chunks, _p(accum), _stream())
-        self._ev("backward", 1)
+        if self.backward_impl == "tc":
+            K.call("ndg_backward_tc", self.n, B, self.tile, _p(qrec), _p(recs.rec_tc), _p(cl.offsets), _p(cl.idx),
+                   _p(accum), _stream())
+            self._ev("backward", 1)
+            K.call("ndg_moments_to_zspace", self.n, recs.Gev, _p(recs.mean64), _p(recs.chol64), _p(recs.eflags),
+                   _p(accum), _stream())
+        else:
+            K.call("ndg_backward", self.n, B, self.tile, _p(qrec), _p(recs.rec), _p(cl.offsets), _p(cl.idx),
+                   _p(cl.chunk_offsets), cl.n_chunks, _p(accum), _stream())
+            self._ev("backward", 1)
         K.call("ndg_epilogue", self.n, mix.G, recs.Gev, mix.amp_mode, _p(mix.params), _p(mix.child), _p(mix.flags),
                _p(recs.eflags), _p(recs.chol64), _p(accum), _p(grads.params), _p(grads.child), _p(grads.stats),
                _p(self.status), _stream())

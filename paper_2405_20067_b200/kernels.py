@@ -39,6 +39,9 @@ SIGNATURES = {
     "ndg_forward": [_I, _L, _I, _P, _P, _P, _P, _P, _F, _L, _P, _P, _P, _P],
     "ndg_loss_finalize": [_L, _P, _P, _P],
     "ndg_backward": [_I, _L, _I, _P, _P, _P, _P, _P, _L, _P, _P],
+    "ndg_backward_tc_supported": [_I],
+    "ndg_backward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _P],
+    "ndg_moments_to_zspace": [_I, _L, _P, _P, _P, _P, _P],
     "ndg_epilogue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "ndg_adam": [_I, _L, _P, _P, _P, _P, _P, _I, _F, _F, _F, _F, _F, _F, _F, _P],
     "ndg_tc_records": [_I, _L, _P, _P, _P, _P, _P, _P],
@@ -84,7 +87,8 @@ class NdgLaunchError(RuntimeError):
 
 # entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
 LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_scan_counts",
-             "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_backward", "ndg_epilogue", "ndg_adam",
+             "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_backward", "ndg_backward_tc",
+             "ndg_moments_to_zspace", "ndg_epilogue", "ndg_adam",
              "ndg_fp32_probe", "ndg_tf32_probe"}
 launch_count = 0
 

@@ -128,6 +128,42 @@ def test_fwd_bwd_parity(cuda, N, G, B, children, amp_mode, regime, fwd):
         assert _rel(st[:, j], ref["stats"][:, j]) < RTOL, f"stat {j}"
 
 
+@pytest.mark.parametrize("N,G,B,children,regime,sigma0", [
+    (2, 200, 1024, True, "R", 0.3),
+    (6, 512, 2048, True, "R", 0.3),
+    (10, 400, 1024, True, "R", 0.3),
+    (10, 600, 2048, False, "C", 0.3),
+    (12, 300, 512, False, "R", 0.4),
+])
+def test_tc_backward_parity(cuda, N, G, B, children, regime, sigma0):
+    """Opt-in tensor-core K7 (ndg_backward_tc + ndg_moments_to_zspace) against the float64 oracle.
+    Its x-space moments lose ~(|x - 1/2| / sigma)^2 x 1e-7 to cancellation, so the
+    parity cases use broad Gaussians; the FP32 K7 (the default) covers sharp ones above."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(N, G, B, children=children, regime=regime, sigma0=sigma0)
+    hp = ndg.HotPath(N, projection_seed=2, backward="tc")
+    assert hp.backward_impl == "tc"
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
+    assert np.array_equal(res.candidates.idx.cpu().numpy(), ref["idx"])
+    _check_grads(N, res.grads.params.cpu().numpy(), ref["grad_parent"], "parent")
+    if children:
+        _check_grads(N, res.grads.child.cpu().numpy(), ref["grad_child"], "child")
+    st = res.grads.stats.cpu().numpy()
+    for j in range(3):
+        assert _rel(st[:, j], ref["stats"][:, j]) < RTOL, f"stat {j}"
+
+
+def test_tc_backward_unsupported_dims_fall_back(cuda):
+    """N > 12 has no tensor-core K7 (the moments do not fit one M=128 GEMM + shared memory): the
+    engine selects the FP32 K7, and the raw entry point refuses loudly."""
+    ndg = _ndg()
+    from paper_2405_20067_b200 import kernels as K
+    assert ndg.HotPath(16, backward="tc").backward_impl == "fp32"
+    with pytest.raises(RuntimeError):
+        K.call("ndg_backward_tc", 16, 256, 256, 0, 0, 0, 0, 0, 0)
+
+
 @pytest.mark.parametrize("fwd", ["fp32", "tc"])
 def test_cfg1_full_size_vs_c_oracle(cuda, fwd):
     """BASELINE.json configs[0] at full size: 6-D, 4096 Gaussians, 16384 queries (64 tiles)."""

@@ -105,9 +105,34 @@ def study(n=10, G=1500, B=4096, regime="R", sigma0=0.15, seed=0):
     S_b1 = np.einsum("gia,gab,gjb->gij", Linv, D2, Linv)
     t_b1 = np.einsum("gia,ga->gi", Linv, M1 - M0[:, None] * m)
     out.update(S_B1=rel(S_b1, S_ref), t_B1=rel(t_b1, t_ref))
+    # B1h (the K7-TC form): features of xhat = [x - 1/2; 1] (the z-GEMM's own features, no per-tile
+    # centring), moments per 128-query block in 3xTF32/fp32, summed in float64, then
+    # S~ = Ahat M Ahat^T and t~ = Ahat M[:, N] with Ahat = [L^-1 | L^-1 (1/2 - m)] in float64.
+    Mh = np.zeros((G, n + 1, n + 1))
+    for b0 in range(0, B, 128):
+        sl = slice(b0, b0 + 128)
+        X = q[sl]
+        d = X[None] - ev.mean[:, None]
+        z = np.einsum("gij,gqj->gqi", Linv, d)
+        g = np.exp(-0.5 * np.sum(z * z, -1))
+        coef = -g * (dpred[sl] @ ev.a.T).T
+        Xh = np.concatenate([X - 0.5, np.ones((X.shape[0], 1))], 1)
+        feats = np.stack([Xh[:, i] * Xh[:, j] for i in range(n + 1) for j in range(i + 1)], 1).astype(np.float32)
+        Mt = split3_matmul(coef.astype(np.float32), feats).astype(np.float64)
+        k = 0
+        for i in range(n + 1):
+            for j in range(i + 1):
+                Mh[:, i, j] += Mt[:, k]
+                if i != j:
+                    Mh[:, j, i] += Mt[:, k]
+                k += 1
+    Ah = np.concatenate([Linv, np.einsum("gij,gj->gi", Linv, 0.5 - ev.mean)[:, :, None]], 2)
+    S_h = np.einsum("gia,gab,gjb->gij", Ah, Mh, Ah)
+    t_h = np.einsum("gia,ga->gi", Ah, Mh[:, :, n])
+    out.update(S_B1h=rel(S_h, S_ref), t_B1h=rel(t_h, t_ref))
     return out
 
 
 if __name__ == "__main__":
-    for regime, s0 in (("R", 0.15), ("C", 0.15), ("R", 0.05), ("C", 0.05)):
+    for regime, s0 in (("R", 0.15), ("C", 0.15), ("R", 0.05), ("C", 0.05), ("R", 0.02), ("C", 0.02)):
         print(study(regime=regime, sigma0=s0), flush=True)
