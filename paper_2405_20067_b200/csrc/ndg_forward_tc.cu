@@ -204,7 +204,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     } else if (warp < kEpi0) {
         // ------------------------------ splitters ----------------------------------------------
         constexpr int NSL = kSplit * 32;
+        constexpr int KU = (C * N * P + NSL - 1) / NSL;      // units per thread of a full chunk
         const int pl = (warp - 2) * 32 + lane;
+        // unit u = pl + k * NSL = (gaussian g, plane p, row i): staging float offset and B-plane byte
+        // offset depend only on (pl, k), so they are computed once
+        int src_off[KU], dst_off[KU];
+#pragma unroll
+        for (int k = 0; k < KU; ++k) {
+            const int u = pl + k * NSL;
+            const int g = u / (N * P), rem = u - g * (N * P);
+            const int p = rem / N, i = rem - p * N;
+            src_off[k] = g * RT + rem * 4;
+            dst_off[k] = p * kPlane + (g * N + i) * 16;
+        }
         for (int c = 0; c < nchunks; ++c) {
             const int sl = c % STG, s = c % kTcStages;
             const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
@@ -216,21 +228,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             uint8_t* bhi = sB + (s * 2 + 0) * P * kPlane;
             uint8_t* blo = sB + (s * 2 + 1) * P * kPlane;
 #ifndef NDG_TCX_NOSPLIT
-#pragma unroll 2
-            for (int u = pl; u < n_in * N * P; u += NSL) {       // unit = (gaussian g, plane p, row i)
-                // records are plane-major ([p][i][4]): consecutive lanes read consecutive 16-B staging
-                // units and write consecutive rows of one plane -> both conflict-free
-                const int g = u / (N * P), rem = u - g * (N * P);
-                const int p = rem / N, i = rem - p * N;
-                const float4 v = *reinterpret_cast<const float4*>(stg + g * RT + rem * 4);
+            // records are plane-major ([p][i][4]): consecutive lanes read consecutive 16-B staging
+            // units and write consecutive rows of one plane -> both conflict-free
+            const int n_units = n_in * N * P;
+#pragma unroll
+            for (int k = 0; k < KU; ++k) {
+                if (pl + k * NSL >= n_units) break;
+                const float4 v = *reinterpret_cast<const float4*>(stg + src_off[k]);
                 float4 hi, lo;
                 tc::split_tf32(v.x, hi.x, lo.x);
                 tc::split_tf32(v.y, hi.y, lo.y);
                 tc::split_tf32(v.z, hi.z, lo.z);
                 tc::split_tf32(v.w, hi.w, lo.w);
-                const int row = g * N + i;
-                *reinterpret_cast<float4*>(bhi + p * kPlane + row * 16) = hi;
-                *reinterpret_cast<float4*>(blo + p * kPlane + row * 16) = lo;
+                *reinterpret_cast<float4*>(bhi + dst_off[k]) = hi;
+                *reinterpret_cast<float4*>(blo + dst_off[k]) = lo;
             }
 #endif
             for (int u = pl; u < n_in; u += NSL)
@@ -269,10 +280,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty_bar[b]);      // TMEM buffer b may be overwritten
 #ifndef NDG_TCX_NOEPI
-#pragma unroll
-            for (int gl = 0; gl < CG; ++gl) {
+            auto gauss = [&](int gl) {
                 const int g = grp * CG + gl;
-                if (g < n_in && (kEpiG == 1 || g < C)) {
+                {
                     float sum;
                     if constexpr ((N & 1) == 0) {
                         float2 acc = make_float2(0.f, 0.f);
@@ -292,6 +302,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     pp[0] = fmaf(gv, av.x, pp[0]);
                     pp[1] = fmaf(gv, av.y, pp[1]);
                     pp[2] = fmaf(gv, av.z, pp[2]);
+                }
+            };
+            if (n_in == C && (kEpiG == 1 || C % kEpiG == 0)) {   // full chunk: no per-Gaussian predicates
+#pragma unroll
+                for (int gl = 0; gl < CG; ++gl) gauss(gl);
+            } else {
+#pragma unroll
+                for (int gl = 0; gl < CG; ++gl) {
+                    const int g = grp * CG + gl;
+                    if (g < n_in && g < C) gauss(gl);
                 }
             }
 #else
