@@ -17,19 +17,7 @@ using namespace ndg;
 
 namespace {
 
-#ifndef NDG_BWD_FFMA2
-#define NDG_BWD_FFMA2 2
-#endif
-#ifndef NDG_BWD_UNROLL
-#define NDG_BWD_UNROLL 1
-#endif
-
 constexpr int kBwdThreads = kBwdChunk;
-constexpr int kBwdUnroll = NDG_BWD_UNROLL;
-
-__host__ __device__ constexpr int rpair_start(int ip) {   // sum_{p<ip} (2p + 1): row-pair offsets
-    return ip * ip;
-}
 
 __host__ __device__ constexpr int srow_start(int i) {   // sum_{r<i} (r/2 + 1): packed S row offsets
     int s = 0;
@@ -37,7 +25,7 @@ __host__ __device__ constexpr int srow_start(int i) {   // sum_{r<i} (r/2 + 1): 
     return s;
 }
 #ifndef NDG_BWD_MINB
-#define NDG_BWD_MINB 3
+#define NDG_BWD_MINB 3   // CTAs per SM the register budget is sized for (N <= 10); tuning builds only
 #endif
 
 template <int N>
@@ -93,87 +81,6 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     mbar_wait(&bar, 0);
     if (!active) return;
 
-#if NDG_BWD_FFMA2 == 1
-    // Packed FP32x2 (FFMA2) layout: z2[kp] = (z~_{2kp}, z~_{2kp+1}); row i of S is kept as
-    // i/2 + 1 pairs (S_i,2jp , S_i,2jp+1); the pair's second slot past the diagonal is scratch.
-    constexpr int NZP = (N + 1) / 2;
-    constexpr int NSP = srow_start(N);
-    float2 Sp[NSP], tv2[NZP];
-    float gA0 = 0.f, gA1 = 0.f, gA2 = 0.f, ls = 0.f, px = 0.f;
-#pragma unroll
-    for (int i = 0; i < NSP; ++i) Sp[i] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int i = 0; i < NZP; ++i) tv2[i] = make_float2(0.f, 0.f);
-
-    for (int q = 0; q < tile; ++q) {
-        float xq[QS];
-        const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
-#pragma unroll
-        for (int v = 0; v < QS / 4; ++v) {
-            const float4 x = q4[v];
-            xq[4 * v] = x.x;
-            xq[4 * v + 1] = x.y;
-            xq[4 * v + 2] = x.z;
-            xq[4 * v + 3] = x.w;
-        }
-        float2 z2[NZP];
-        z2[NZP - 1] = make_float2(0.f, 0.f);            // pad slot when N is odd
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            float2 acc = make_float2(fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]), 0.f);
-#pragma unroll
-            for (int kp = 0; kp < i / 2; ++kp)
-                acc = __ffma2_rn(make_float2(r[rec_l(N, i, 2 * kp)], r[rec_l(N, i, 2 * kp) + 1]), z2[kp], acc);
-            if (i & 1) acc.x = fmaf(r[rec_l(N, i, i - 1)], z2[(i - 1) / 2].x, acc.x);
-            const float zi = acc.x + acc.y;
-            if (i & 1) z2[i / 2].y = zi;
-            else z2[i / 2].x = zi;
-        }
-        float2 ss = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int kp = 0; kp < NZP; ++kp) ss = __ffma2_rn(z2[kp], z2[kp], ss);
-        const float s2 = ss.x + ss.y;
-        const float g = ex2_neg(s2);
-        const float dp0 = xq[N], dp1 = xq[N + 1], dp2 = xq[N + 2], ell = xq[N + 3];
-        const float h = fmaf(dp2, r[A0 + 2], fmaf(dp1, r[A0 + 1], dp0 * r[A0]));
-        const float wgt = g * h;
-        float2 u2[NZP];
-#pragma unroll
-        for (int kp = 0; kp < NZP; ++kp) {
-            u2[kp] = __fmul2_rn(make_float2(wgt, wgt), z2[kp]);
-            tv2[kp] = __fadd2_rn(tv2[kp], u2[kp]);
-        }
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const float ui = (i & 1) ? u2[i / 2].y : u2[i / 2].x;
-#pragma unroll
-            for (int jp = 0; jp <= i / 2; ++jp)
-                Sp[srow_start(i) + jp] = __ffma2_rn(make_float2(ui, ui), z2[jp], Sp[srow_start(i) + jp]);
-        }
-        gA0 = fmaf(g, dp0, gA0);
-        gA1 = fmaf(g, dp1, gA1);
-        gA2 = fmaf(g, dp2, gA2);
-        ls = fmaf(g, ell, ls);
-        px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
-    }
-
-    double* out = accum + e * A;
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-#pragma unroll
-        for (int j = 0; j <= i; ++j) {
-            const float2 v = Sp[srow_start(i) + j / 2];
-            atomicAdd(out + tri(i, j), (double)((j & 1) ? v.y : v.x));
-        }
-#pragma unroll
-    for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
-    atomicAdd(out + acc_tail(N), (double)gA0);
-    atomicAdd(out + acc_tail(N) + 1, (double)gA1);
-    atomicAdd(out + acc_tail(N) + 2, (double)gA2);
-    atomicAdd(out + acc_tail(N) + 3, (double)ls);
-    atomicAdd(out + acc_tail(N) + 4, (double)px);
-    atomicAdd(out + acc_tail(N) + 5, (double)tile);
-#elif NDG_BWD_FFMA2 == 2
     // scalar forward substitution (no added dependencies), packed FFMA2 for u = w z~, t += u and the
     // outer-product rows S_i,(2jp, 2jp+1) += u_i (z~_2jp, z~_2jp+1)
     constexpr int NZP = (N + 1) / 2;
@@ -184,7 +91,6 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     for (int i = 0; i < NSP; ++i) Sp[i] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < NZP; ++i) tv2[i] = make_float2(0.f, 0.f);
-#pragma unroll kBwdUnroll
     for (int q = 0; q < tile; ++q) {
         float xq[QS];
         const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
@@ -248,150 +154,6 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     atomicAdd(out + acc_tail(N) + 3, (double)ls);
     atomicAdd(out + acc_tail(N) + 4, (double)px);
     atomicAdd(out + acc_tail(N) + 5, (double)tile);
-#elif NDG_BWD_FFMA2 == 3
-    // scalar forward substitution (no added dependencies); packed FFMA2 for u = w z~, t += u and the
-    // outer product by ROW pairs: (S_i,j , S_i+1,j) += z~_j * (u_i, u_i+1) for even i, j <= i, plus the
-    // diagonal S_i+1,i+1 -- exactly the lower triangle, no scratch slots.
-    constexpr int NZP = (N + 1) / 2;
-    constexpr int NSP = rpair_start(NZP);
-    float2 Sp[NSP], tv2[NZP];
-    float Sd[NZP];
-#pragma unroll
-    for (int i = 0; i < NZP; ++i) Sd[i] = 0.f;
-    float gA0 = 0.f, gA1 = 0.f, gA2 = 0.f, ls = 0.f, px = 0.f;
-#pragma unroll
-    for (int i = 0; i < NSP; ++i) Sp[i] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int i = 0; i < NZP; ++i) tv2[i] = make_float2(0.f, 0.f);
-#pragma unroll kBwdUnroll
-    for (int q = 0; q < tile; ++q) {
-        float xq[QS];
-        const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
-#pragma unroll
-        for (int v = 0; v < QS / 4; ++v) {
-            const float4 x = q4[v];
-            xq[4 * v] = x.x;
-            xq[4 * v + 1] = x.y;
-            xq[4 * v + 2] = x.z;
-            xq[4 * v + 3] = x.w;
-        }
-        float2 z2[NZP];
-        z2[NZP - 1] = make_float2(0.f, 0.f);
-        float s2 = 0.f;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]);
-#pragma unroll
-            for (int k = 0; k < i; ++k) acc = fmaf(r[rec_l(N, i, k)], (k & 1) ? z2[k / 2].y : z2[k / 2].x, acc);
-            if (i & 1) z2[i / 2].y = acc;
-            else z2[i / 2].x = acc;
-            s2 = fmaf(acc, acc, s2);
-        }
-        const float g = ex2_neg(s2);
-        const float dp0 = xq[N], dp1 = xq[N + 1], dp2 = xq[N + 2], ell = xq[N + 3];
-        const float h = fmaf(dp2, r[A0 + 2], fmaf(dp1, r[A0 + 1], dp0 * r[A0]));
-        const float wgt = g * h;
-        float2 u2[NZP];
-#pragma unroll
-        for (int kp = 0; kp < NZP; ++kp) {
-            u2[kp] = __fmul2_rn(make_float2(wgt, wgt), z2[kp]);
-            tv2[kp] = __fadd2_rn(tv2[kp], u2[kp]);
-        }
-#pragma unroll
-        for (int ip = 0; ip < NZP; ++ip) {
-#pragma unroll
-            for (int j = 0; j <= 2 * ip; ++j) {
-                const float zj = (j & 1) ? z2[j / 2].y : z2[j / 2].x;
-                Sp[rpair_start(ip) + j] = __ffma2_rn(make_float2(zj, zj), u2[ip], Sp[rpair_start(ip) + j]);
-            }
-            Sd[ip] = fmaf(u2[ip].y, z2[ip].y, Sd[ip]);
-        }
-        gA0 = fmaf(g, dp0, gA0);
-        gA1 = fmaf(g, dp1, gA1);
-        gA2 = fmaf(g, dp2, gA2);
-        ls = fmaf(g, ell, ls);
-        px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
-    }
-
-    double* out = accum + e * A;
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-#pragma unroll
-        for (int j = 0; j <= i; ++j) {
-            const int ip = i / 2;
-            const float v = (i & 1) ? (j == i ? Sd[ip] : Sp[rpair_start(ip) + j].y) : Sp[rpair_start(ip) + j].x;
-            atomicAdd(out + tri(i, j), (double)v);
-        }
-#pragma unroll
-    for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
-    atomicAdd(out + acc_tail(N), (double)gA0);
-    atomicAdd(out + acc_tail(N) + 1, (double)gA1);
-    atomicAdd(out + acc_tail(N) + 2, (double)gA2);
-    atomicAdd(out + acc_tail(N) + 3, (double)ls);
-    atomicAdd(out + acc_tail(N) + 4, (double)px);
-    atomicAdd(out + acc_tail(N) + 5, (double)tile);
-#else
-    // scalar FP32: one FFMA per multiply-add (the packed variant adds pad work)
-    float S[P], tv[N], gA[3], ls = 0.f, px = 0.f;
-#pragma unroll
-    for (int i = 0; i < P; ++i) S[i] = 0.f;
-#pragma unroll
-    for (int i = 0; i < N; ++i) tv[i] = 0.f;
-    gA[0] = gA[1] = gA[2] = 0.f;
-
-#pragma unroll kBwdUnroll
-    for (int q = 0; q < tile; ++q) {
-        float xq[QS];
-        const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
-#pragma unroll
-        for (int v = 0; v < QS / 4; ++v) {
-            const float4 x = q4[v];
-            xq[4 * v] = x.x;
-            xq[4 * v + 1] = x.y;
-            xq[4 * v + 2] = x.z;
-            xq[4 * v + 3] = x.w;
-        }
-        float z[N];
-        float s2 = 0.f;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]);
-#pragma unroll
-            for (int k = 0; k < i; ++k) acc = fmaf(r[rec_l(N, i, k)], z[k], acc);
-            z[i] = acc;
-            s2 = fmaf(acc, acc, s2);
-        }
-        const float g = ex2_neg(s2);
-        const float dp0 = xq[N], dp1 = xq[N + 1], dp2 = xq[N + 2], ell = xq[N + 3];
-        const float h = fmaf(dp2, r[A0 + 2], fmaf(dp1, r[A0 + 1], dp0 * r[A0]));
-        const float wgt = g * h;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const float u = wgt * z[i];
-            tv[i] += u;
-#pragma unroll
-            for (int j = 0; j <= i; ++j) S[tri(i, j)] = fmaf(u, z[j], S[tri(i, j)]);
-        }
-        gA[0] = fmaf(g, dp0, gA[0]);
-        gA[1] = fmaf(g, dp1, gA[1]);
-        gA[2] = fmaf(g, dp2, gA[2]);
-        ls = fmaf(g, ell, ls);
-        px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
-    }
-
-
-    double* out = accum + e * A;
-#pragma unroll
-    for (int i = 0; i < P; ++i) atomicAdd(out + i, (double)S[i]);
-#pragma unroll
-    for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)tv[i]);
-    atomicAdd(out + acc_tail(N), (double)gA[0]);
-    atomicAdd(out + acc_tail(N) + 1, (double)gA[1]);
-    atomicAdd(out + acc_tail(N) + 2, (double)gA[2]);
-    atomicAdd(out + acc_tail(N) + 3, (double)ls);
-    atomicAdd(out + acc_tail(N) + 4, (double)px);
-    atomicAdd(out + acc_tail(N) + 5, (double)tile);
-#endif
 }
 
 template <int N>
