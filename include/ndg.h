@@ -159,6 +159,17 @@ int ndg_moments_to_zspace(int n, int64_t Gev, const double* mean64, const double
                           double* accum, void* stream);
 
 /*
+ * Diagnostic (not on the training path): brute_force_active for every tile as a
+ * bit-mask [T][ceil(Gev/32)] (+ per-tile popcounts, zeroed by the caller): bit (t, e) = 1 iff a live,
+ * non-degenerate evaluated Gaussian e has |z|^2 <= max_s2 (float64 forward substitution) at some query
+ * of tile t, i.e. eval_gaussian >= epsilon with max_s2 = -2 ln epsilon. The culling ablation
+ * (cmd_bench_cull) counts false culls against it.
+ */
+int ndg_active_mask(int n, int64_t B, int tile, const float* queries, const double* mean64, const double* chol64,
+                    const uint8_t* eflags, int64_t Gev, double max_s2, uint32_t* mask, int64_t* counts,
+                    void* stream);
+
+/*
  * K8 epilogue. Replaces the tail of `backward`: raw-parameter gradients of parents
  * and live children including the child->parent cross terms; stats[Gev][3] =
  * (loss share, gradient proxy, pairs). Non-finite gradients -> status NONFINITE_GRADIENT.

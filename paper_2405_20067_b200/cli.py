@@ -2,13 +2,22 @@
 
     ndgauss fit  --config PATH --out DIR [--resume CKPT]
     ndgauss eval --ckpt PATH (--queries PATH | --grid SPEC) --out DIR [--ref PATH] [--no-cull]
+    ndgauss bench-cull --config PATH --out CSV
 
 fit writes metrics.csv (iteration,loss,n_components,culled_fraction,ms_per_iter) and a checkpoint
 every phase and at the end; exit 0 on completion, 2 on a config error, 3 on TrainingAborted
 (SPEC.md:514-515). eval writes the predictions as an NDGT file (and PFM/PPM for a 2-D grid slice)
 and reports rel-L2 / PSNR against --ref. --grid SPEC = "d0,d1:W,H[:v]" evaluates the
 2-D slice over dims d0, d1 at W x H points with the other dims fixed at v (default 0.5).
-`gradcheck` and `bench-cull` are not provided.
+bench-cull (the paper's culling ablation) sweeps k x multiplier x tile size over a
+seeded synthetic workload ([bench] config section) and writes one CSV row per point: cull fraction,
+false culls = (tile, Gaussian) pairs brute_force_active at the 3-sigma level epsilon = exp(-4.5)
+(float64, on the device) that the cull dropped, max |pred_culled - pred_brute|, and
+the wall-clock of culled vs brute-force evaluation. Multiplier >= 3 rows have no false culls by
+Cauchy-Schwarz; multiplier 1 rows show the paper's artifact regime. (The culled tail still moves pred
+by up to exp(-m^2/2) * sum |a| of the dropped Gaussians, so max_abs_err is reported, not bounded by
+1e-6: DESIGN.md §5.)
+`gradcheck` is not provided.
 """
 from __future__ import annotations
 
@@ -155,6 +164,84 @@ def cmd_eval(args) -> int:
     return 0
 
 
+_POPCOUNT = None
+
+
+def _popcount(words) -> int:
+    """Number of set bits in an int32 tensor (byte lookup table)."""
+    import torch
+    global _POPCOUNT
+    if _POPCOUNT is None or _POPCOUNT.device != words.device:
+        _POPCOUNT = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int64, device=words.device)
+    return int(_POPCOUNT[words.contiguous().view(torch.uint8).long()].sum())
+
+
+def cmd_bench_cull(args) -> int:
+    import time
+    import torch
+    from . import datasets as D
+    from .engine import HotPath
+    from .gmm import Mixture
+    try:
+        cfg = nio.parse_config(open(args.config).read())
+    except ConfigError as e:
+        print(f"config error: {e}", file=sys.stderr)
+        return 2
+    b = cfg.get("bench", {})
+    aslist = lambda v, d: [v] if isinstance(v, (int, float)) else (list(v) if v is not None else d)  # noqa: E731
+    n = int(cfg.get("data", {}).get("n_dims", 10))
+    G, B = int(b.get("gaussians", 10000)), int(b.get("queries", 1 << 16))
+    regime, seed, reps = str(b.get("regime", "C")), int(b.get("seed", 0)), int(b.get("reps", 3))
+    eps = float(b.get("epsilon", math.exp(-4.5)))
+    ks = [int(x) for x in aslist(b.get("k_list"), [4, 8, 16, 32])]
+    mults = [float(x) for x in aslist(b.get("multiplier_list"), [1, 2, 3, 4])]
+    tiles = [int(x) for x in aslist(b.get("tile_list"), [64, 256])]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    mix_np, _ = D.synthetic_mixture(n, G, seed=seed, sigma0=b.get("sigma0"))
+    mix = Mixture.from_arrays(n, 0, **mix_np, device=dev)
+    qd = torch.from_numpy(D.synthetic_queries(n, B, seed=seed + 1, regime=regime)).to(dev)
+
+    def timed(fn):
+        fn()                                   # warm-up (also builds the per-N kernel attributes)
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        return out, 1e3 * sorted(ts)[len(ts) // 2]
+
+    rows = []
+    for tile in tiles:
+        if B % tile:
+            print(f"queries ({B}) must be a multiple of every tile size ({tile})", file=sys.stderr)
+            return 2
+        hb = HotPath(n, tile_size=tile, device=dev)
+        pred_ref, ms_brute = timed(lambda: hb.evaluate(mix, qd, cull=False))
+        recs = hb.activate(mix)
+        T = B // tile
+        live_pairs = T * int((recs.eflags & 1).sum())
+        active, acount = hb.brute_force_active(qd, recs, eps)
+        n_active = int(acount.sum())
+        for mult in mults:
+            for k in ks:
+                hp = HotPath(n, k=k, multiplier=mult, tile_size=tile, projection_seed=seed + 2, device=dev)
+                pred, ms_cull = timed(lambda: hp.evaluate(mix, qd, cull=True))
+                cl = hp.cull(hp.tile_bounds(qd), hp.project(recs))
+                false_culls = _popcount(active & ~cl.mask)
+                err = float((pred - pred_ref).abs().max()) if B else 0.0
+                rows.append(dict(k=k, multiplier=mult, tile_size=tile, cull_fraction=1.0 - cl.n_pairs_tiles / max(1, live_pairs),
+                                 kept_pairs=cl.n_pairs_tiles * tile, active_pairs=n_active * tile, false_culls=false_culls,
+                                 max_abs_err=err, ms_culled=ms_cull, ms_brute=ms_brute, speedup=ms_brute / ms_cull))
+    cols = list(rows[0].keys()) if rows else []
+    with open(args.out, "w") as f:
+        f.write(",".join(cols) + "\n")
+        for r in rows:
+            f.write(",".join(f"{r[c]:.6g}" if isinstance(r[c], float) else str(r[c]) for c in cols) + "\n")
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="ndgauss")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -170,9 +257,12 @@ def main(argv=None) -> int:
     e.add_argument("--out", required=True)
     e.add_argument("--ref")
     e.add_argument("--no-cull", action="store_true")
+    bc = sub.add_parser("bench-cull")
+    bc.add_argument("--config", required=True)
+    bc.add_argument("--out", required=True)
     args = ap.parse_args(argv)
     try:
-        return cmd_fit(args) if args.cmd == "fit" else cmd_eval(args)
+        return {"fit": cmd_fit, "eval": cmd_eval, "bench-cull": cmd_bench_cull}[args.cmd](args)
     except NdgError as err:
         print(f"error: {err}", file=sys.stderr)
         return 1

@@ -112,6 +112,7 @@ class CandidateLists:
     chunk_offsets: torch.Tensor
     n_pairs_tiles: int        # sum over tiles of |cand(tile)|
     n_chunks: int
+    mask: torch.Tensor = None  # [T, ceil(Gev/32)] int32 bit-words the CSR was compacted from
 
     @property
     def T(self):
@@ -281,6 +282,22 @@ class HotPath:
         counts = live.sum().to(torch.int64).repeat(T)
         return self._finish_lists(T, Gev, counts, mask)
 
+    def brute_force_active(self, queries, recs: EvalRecords, epsilon: float):
+        """brute_force_active for every tile, in float64 on the device: returns
+        (mask [T, ceil(Gev/32)] int32 bit-words, counts [T] int64) of the evaluated Gaussians with
+        eval_gaussian >= epsilon at some query of the tile."""
+        B = int(queries.shape[0])
+        if B % self.tile:
+            raise ValueError("batch size must be a multiple of tile_size (SPEC.md:441-442)")
+        T, Gev = B // self.tile, recs.Gev
+        W = (Gev + 31) // 32
+        mask = torch.zeros(T, W, dtype=torch.int32, device=self.device)
+        counts = torch.zeros(T, dtype=torch.int64, device=self.device)
+        max_s2 = float("inf") if epsilon <= 0 else -2.0 * math.log(epsilon)
+        K.call("ndg_active_mask", self.n, B, self.tile, _p(queries), _p(recs.mean64), _p(recs.chol64), _p(recs.eflags),
+               Gev, max_s2, _p(mask), _p(counts), _stream())
+        return mask, counts
+
     def _finish_lists(self, T, Gev, counts, mask) -> CandidateLists:
         offsets = torch.empty(T + 1, dtype=torch.int64, device=self.device)
         chunk_off = torch.empty(T + 1, dtype=torch.int64, device=self.device)
@@ -289,7 +306,7 @@ class HotPath:
         nnz, nchunks = int(tot[0]), int(tot[1])
         idx = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.device)
         K.call("ndg_cull_compact", T, Gev, _p(mask), _p(offsets), _p(idx), _stream())
-        return CandidateLists(offsets, idx[:nnz], chunk_off, nnz, nchunks)
+        return CandidateLists(offsets, idx[:nnz], chunk_off, nnz, nchunks, mask)
 
     # -- K5 + K6 ---------------------------------------------------------------------------
     def forward(self, queries, recs: EvalRecords, cl: CandidateLists, targets=None, n_total=None):

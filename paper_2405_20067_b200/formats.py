@@ -23,11 +23,16 @@ SECTIONS = {
                 "amp_mode", "loss_eps"),
     "culling": ("k", "multiplier", "tile_size", "cull"),
     "data": ("target", "n_dims", "target_components", "target_seed"),
+    # cmd_bench_cull: synthetic workload + the sweep (comma-separated lists)
+    "bench": ("gaussians", "queries", "regime", "sigma0", "seed", "k_list", "multiplier_list", "tile_list", "reps",
+              "epsilon"),
 }
 
 
 def _convert(raw: str, line: int, field: str):
     v = raw.strip()
+    if "," in v:                                   # list value, e.g. k_list = 4, 8, 16, 32
+        return [_convert(x, line, field) for x in v.split(",") if x.strip()]
     if v.lower() in ("true", "false"):
         return v.lower() == "true"
     if v.lower() in ("brightness", "opacity"):

@@ -21,6 +21,16 @@ def test_config_parse_and_errors():
     assert e.value.line == 1
 
 
+def test_config_bench_section_lists():
+    cfg = F.parse_config("[data]\nn_dims = 10\n[bench]\ngaussians = 20000\nregime = C\n"
+                         "k_list = 4, 8, 16, 32\nmultiplier_list = 1, 2.5, 3\ntile_list = 64\n")
+    b = cfg["bench"]
+    assert b["k_list"] == [4, 8, 16, 32] and b["multiplier_list"] == [1, 2.5, 3]
+    assert b["tile_list"] == 64 and b["regime"] == "C" and b["gaussians"] == 20000
+    with pytest.raises(ConfigError):
+        F.parse_config("[bench]\nk_list = 4, $\n")
+
+
 def test_ndgt_roundtrip_and_errors(tmp_path):
     rng = np.random.default_rng(0)
     q = rng.random((37, 6)).astype(np.float32)

@@ -40,3 +40,32 @@ def test_fit_eval_resume(cuda, tmp_path):
                      "--ref", str(tmp_path / "q.ndgt"), "--out", str(ev2), "--no-cull"]) == 0
     _, p2, _ = F.read_ndgt(ev2 / "pred.ndgt")
     assert p2.shape == (100, 3) and np.all(np.isfinite(p2))
+
+
+def test_bench_cull_ablation(cuda, tmp_path):
+    """cmd_bench_cull on a small inference-shaped workload: multiplier 3 culls
+    nothing active at the 3-sigma level (0 false culls); multiplier 1 culls contributing Gaussians
+    (the paper's artifact regime) and moves the output far more; more projection vectors never keep
+    more pairs."""
+    from paper_2405_20067_b200 import cli
+    cfgp = tmp_path / "bc.cfg"
+    cfgp.write_text("[data]\nn_dims = 10\n[bench]\ngaussians = 4000\nqueries = 16384\nregime = C\n"
+                    "k_list = 4, 16\nmultiplier_list = 1, 3\ntile_list = 64, 256\nreps = 1\n")
+    out = tmp_path / "bc.csv"
+    assert cli.main(["bench-cull", "--config", str(cfgp), "--out", str(out)]) == 0
+    lines = out.read_text().strip().splitlines()
+    hdr = lines[0].split(",")
+    rows = [dict(zip(hdr, ln.split(","))) for ln in lines[1:]]
+    assert len(rows) == 2 * 2 * 2
+    for r in rows:
+        if float(r["multiplier"]) == 3:
+            assert int(r["false_culls"]) == 0
+        else:
+            assert int(r["false_culls"]) > 0
+    err = {m: max(float(r["max_abs_err"]) for r in rows if float(r["multiplier"]) == m) for m in (1.0, 3.0)}
+    assert err[3.0] < 0.1 * err[1.0]
+    for tile in ("64", "256"):
+        for m in ("1", "3"):
+            kept = {int(r["k"]): int(r["kept_pairs"]) for r in rows
+                    if r["tile_size"] == tile and float(r["multiplier"]) == float(m)}
+            assert kept[16] <= kept[4]

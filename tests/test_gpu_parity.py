@@ -164,6 +164,29 @@ def test_tc_backward_unsupported_dims_fall_back(cuda):
         K.call("ndg_backward_tc", 16, 256, 256, 0, 0, 0, 0, 0, 0)
 
 
+@pytest.mark.parametrize("N,regime", [(2, "R"), (6, "C"), (10, "C")])
+def test_brute_force_active_mask_vs_oracle(cuda, N, regime):
+    """ndg_active_mask == oracle brute_force_active per tile, and the cull keeps a
+    superset of it at multiplier 3 (conservativeness)."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(N, 300, 1024, children=True, regime=regime)
+    hp = ndg.HotPath(N, projection_seed=2)
+    recs = hp.activate(mix)
+    qd = torch.from_numpy(q).cuda()
+    eps = float(np.exp(-4.5))
+    mask, counts = hp.brute_force_active(qd, recs, eps)
+    m = mask.cpu().numpy().view(np.uint32)
+    ev = O.build_eval_set(om)
+    for tt in range(1024 // 256):
+        want = O.brute_force_active(q[tt * 256:(tt + 1) * 256], ev, eps)
+        got = np.flatnonzero((m[tt][np.arange(ev.Gev) // 32] >> (np.arange(ev.Gev) % 32)) & 1)
+        assert np.array_equal(got, want), tt
+        assert int(counts[tt]) == want.size
+    cl = hp.cull(hp.tile_bounds(qd), hp.project(recs))
+    kept = cl.mask.cpu().numpy().view(np.uint32)
+    assert not np.any(m & ~kept)
+
+
 @pytest.mark.parametrize("fwd", ["fp32", "tc"])
 def test_cfg1_full_size_vs_c_oracle(cuda, fwd):
     """BASELINE.json configs[0] at full size: 6-D, 4096 Gaussians, 16384 queries (64 tiles)."""
