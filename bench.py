@@ -279,7 +279,8 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
         total_ms = float(tt)
     out = dict(total_ms=total_ms, ms_per_step=total_ms / steps, value=a.batch * world * steps / (total_ms * 1e-3),
                kept=statistics.mean(kept), pairs=statistics.mean(pairs), fwd_ms=fwd_ms, bwd_ms=bwd_ms,
-               launches=launches, clocks=clk, loss=res.loss, sigma0=s0, fwd_impl=hp.forward_impl)
+               launches=launches, clocks=clk, loss=res.loss, sigma0=s0, fwd_impl=hp.last_forward_impl,
+               bwd_impl=hp.last_backward_impl)
 
     if measure_e2e:
         qh = torch.from_numpy(q).pin_memory()

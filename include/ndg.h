@@ -119,9 +119,12 @@ int ndg_forward(int n, int64_t B, int tile, const float* queries, const float* t
 
 /* Tensor-core records (float32 [Gev][N*pad8(N+1) + 4], rows stored plane-major [K/4][N][4]):
  * Ahat_e = [C L^-1 | C L^-1 (1/2 - m)] from K1's
- * float64 factor (the B operand of the tcgen05 z-GEMM), followed by the colour a[3] and a pad. */
+ * float64 factor (the B operand of the tcgen05 z-GEMM), followed by the colour a[3] and a pad.
+ * cond (optional, 3 doubles zeroed by the caller) receives [max, sum of squares, count] over live,
+ * non-degenerate e of B_e = max_i (1/2 sum_k |Ahat_ik| + |bias_i|), the conditioning of the z-GEMM
+ * (engine.py keeps very sharp mixtures on the FP32 pipe with it). */
 int ndg_tc_records(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
-                   const float* rec, float* rec_tc, void* stream);
+                   const float* rec, float* rec_tc, double* cond, void* stream);
 
 /* K5+K6 on the tensor cores (tcgen05 kind::tf32, 3xTF32): same contract as ndg_forward, plus the
  * rec_tc records; tile must be <= 256. */

@@ -399,9 +399,17 @@ int launch_forward_tc(int64_t B, int tile, const float* q, const float* tgt, con
 // plane-major ([K/4][N][4], the order the B operand's planes need), then a[3] and a pad;
 // row i = [C (L^-1)_i0 .. C (L^-1)_i,N-1 | C (L^-1 (1/2 - m))_i | 0 ...], computed in float64 from
 // K1's activated / composed factor (forward substitution on the identity, never forming V^-1).
+//
+// Conditioning (cond, optional, 3 doubles zeroed by the caller): B_e = max_i (1/2 sum_k<N |Ahat_ik| +
+// |Ahat_iN|) bounds the magnitude of the terms the z-GEMM adds for any query in [0,1]^N
+// (|x - 1/2| <= 1/2). z~ itself is O(1) where g matters, so the fp32-accumulated 3xTF32 GEMM loses
+// ~1e-7 * B_e absolute to cancellation. cond = [max_e B_e, sum_e B_e^2, count] over live,
+// non-degenerate e; the host compares the RMS with the measured-safe bound (engine.py) and evaluates
+// the step on the FP32 pipe when it is exceeded (very sharp mixtures, sigma ~ 1e-3).
 __global__ void tc_records_kernel(int n, int64_t Gev, const double* __restrict__ mean64,
                                   const double* __restrict__ chol64, const uint8_t* __restrict__ eflags,
-                                  const float* __restrict__ rec, float* __restrict__ rec_tc) {
+                                  const float* __restrict__ rec, float* __restrict__ rec_tc,
+                                  double* __restrict__ cond) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= Gev) return;
     const int P = n_chol(n), K = tc_k(n), RT = tc_rec_floats(n);
@@ -419,25 +427,35 @@ __global__ void tc_records_kernel(int n, int64_t Gev, const double* __restrict__
         }
     // plane-major: element (row i, column k) at ((k / 4) * n + i) * 4 + k % 4
     auto at = [&](int i, int k) -> float& { return out[((k / 4) * n + i) * 4 + (k & 3)]; };
+    double bound = 0.0;
     for (int i = 0; i < n; ++i) {
-        double bias = 0.0;
+        double bias = 0.0, lin = 0.0;
         for (int j = 0; j <= i; ++j) {
             const double w = kC * W[tri(i, j)];
             at(i, j) = (float)w;
             bias += w * (0.5 - mean64[e * n + j]);
+            lin += fabs(w);
         }
         at(i, n) = (float)bias;
+        bound = fmax(bound, 0.5 * lin + fabs(bias));
+    }
+    if (cond && !(eflags[e] & 2)) {
+        const double b = isfinite(bound) ? bound : 1.0e300;
+        // positive doubles order like their bit patterns
+        atomicMax(reinterpret_cast<unsigned long long*>(cond), (unsigned long long)__double_as_longlong(b));
+        atomicAdd(cond + 1, b * b);
+        atomicAdd(cond + 2, 1.0);
     }
 }
 
 }  // namespace
 
 extern "C" int ndg_tc_records(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
-                              const float* rec, float* rec_tc, void* stream) {
+                              const float* rec, float* rec_tc, double* cond, void* stream) {
     if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
     if (Gev == 0) return NDG_OK;
     tc_records_kernel<<<(unsigned)((Gev + 127) / 128), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        n, Gev, mean64, chol64, eflags, rec, rec_tc);
+        n, Gev, mean64, chol64, eflags, rec, rec_tc, cond);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }

@@ -85,6 +85,17 @@ class EvalRecords:
     chol64: torch.Tensor     # [Gev, P] float64 packed lower factor (composed for children)
     eflags: torch.Tensor     # [Gev] uint8: bit0 live, bit1 degenerate
     rec_tc: torch.Tensor = None   # [Gev, N*pad8(N+1) + 4] float32 Ahat records + colour (tensor-core forward)
+    tc_cond: torch.Tensor = None   # [3] float64: [max, sum of squares, count] of B_e (ndg_tc_records)
+    tc_cond_host: tuple = None     # read back with the step's one mid-pipeline sync
+
+    def tc_conditioning(self) -> float:
+        """RMS over live Gaussians of B_e, the z-GEMM's conditioning (inf without tensor-core records)."""
+        if self.tc_cond_host is None:
+            if self.tc_cond is None:
+                return float("inf")
+            self.tc_cond_host = tuple(self.tc_cond.cpu().tolist())
+        mx, ss, cnt = self.tc_cond_host
+        return math.sqrt(ss / cnt) if cnt > 0 else 0.0
 
 
 @dataclass
@@ -191,12 +202,16 @@ class HotPath:
         self.forward_impl = forward or os.environ.get("NDG_FORWARD", "tc")
         if self.forward_impl not in ("tc", "fp32"):
             raise ValueError("forward must be 'tc' or 'fp32'")
+        if self.forward_impl == "tc" and self.tile > 256:
+            self.forward_impl = "fp32"      # the tcgen05 K5 covers tiles of up to two 128-query halves
         # K7 implementation: "fp32" = FP32-pipe pair loop (default); "tc" = tcgen05 z-GEMM + moments GEMM
         # (N <= 12, opt-in: no faster and only marginally within 1e-4)
         bwd = backward or os.environ.get("NDG_BACKWARD", "fp32")
         if bwd not in ("tc", "fp32"):
             raise ValueError("backward must be 'tc' or 'fp32'")
         self.backward_impl = "tc" if bwd == "tc" and K.load().ndg_backward_tc_supported(self.n) else "fp32"
+        self._recs = None    # the last activation: its conditioning bound rides on the cull's read-back
+        self.last_forward_impl = self.last_backward_impl = None   # what the last step ran
         self.events = None   # when a dict: {"forward": [(start, end), ...], "backward": [...]} CUDA events
 
     def enable_kernel_timing(self, on: bool = True):
@@ -231,8 +246,30 @@ class HotPath:
         if self.forward_impl == "tc" or self.backward_impl == "tc":
             kk = ((n + 1 + 7) // 8) * 8
             rec_tc = torch.empty(Gev, n * kk + 4, dtype=torch.float32, device=dev)
-            K.call("ndg_tc_records", n, Gev, _p(mean64), _p(chol64), _p(eflags), _p(rec), _p(rec_tc), _stream())
-        return EvalRecords(Gev, rec, mean64, chol64, eflags, rec_tc)
+            cond = torch.zeros(3, dtype=torch.float64, device=dev)
+            K.call("ndg_tc_records", n, Gev, _p(mean64), _p(chol64), _p(eflags), _p(rec), _p(rec_tc), _p(cond),
+                   _stream())
+            recs = EvalRecords(Gev, rec, mean64, chol64, eflags, rec_tc, cond)
+        else:
+            recs = EvalRecords(Gev, rec, mean64, chol64, eflags)
+        self._recs = recs
+        return recs
+
+    # Largest z-GEMM conditioning (RMS over live Gaussians of B_e, ndg_tc_records) each tensor-core
+    # kernel runs at; above it the step uses the FP32-pipe kernel with the same contract. K5: cfg2 sits
+    # at 35, sigma 0.02 at 256 (parity 4.4e-5), the N=1 sigma 8e-4 mixture of tests/test_gpu_fuzz.py
+    # at 842 (2.3e-4, out of tolerance). The moments K7 loses ~B^2 and is held to broad mixtures.
+    TC_FORWARD_MAX_BOUND = 200.0      # RMS of B_e; error ~2e-7 * RMS (measured 4.4e-5 @ 256, 2.3e-4 @ 842)
+    TC_BACKWARD_MAX_BOUND = 20.0      # moments K7: error ~8e-8 * RMS^2 (9.7e-5 vs the FP32 K7 @ 35)
+
+    def forward_tc_ok(self, recs: EvalRecords) -> bool:
+        """Whether this step's K5 runs on the tensor cores (else the FP32-pipe K5, same contract)."""
+        return (self.forward_impl == "tc" and recs.rec_tc is not None
+                and recs.tc_conditioning() <= self.TC_FORWARD_MAX_BOUND)
+
+    def backward_tc_ok(self, recs: EvalRecords) -> bool:
+        return (self.backward_impl == "tc" and recs.rec_tc is not None
+                and recs.tc_conditioning() <= self.TC_BACKWARD_MAX_BOUND)
 
     # -- K2 --------------------------------------------------------------------------------
     def project(self, recs: EvalRecords) -> ProjectedBounds:
@@ -302,8 +339,15 @@ class HotPath:
         offsets = torch.empty(T + 1, dtype=torch.int64, device=self.device)
         chunk_off = torch.empty(T + 1, dtype=torch.int64, device=self.device)
         K.call("ndg_scan_counts", T, _p(counts), _p(offsets), _p(chunk_off), _stream())
-        tot = torch.stack([offsets[T], chunk_off[T]]).cpu()   # the step's one mid-pipeline sync: sizes idx
+        vals = [offsets[T:T + 1], chunk_off[T:T + 1]]
+        recs = self._recs if (self._recs is not None and self._recs.tc_cond is not None
+                              and self._recs.tc_cond_host is None) else None
+        if recs is not None:
+            vals.append(recs.tc_cond.view(torch.int64))
+        tot = torch.cat(vals).cpu()          # the step's one mid-pipeline sync: sizes idx (+ K5's conditioning)
         nnz, nchunks = int(tot[0]), int(tot[1])
+        if recs is not None:
+            recs.tc_cond_host = tuple(tot[2:5].view(torch.float64).tolist())
         idx = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.device)
         K.call("ndg_cull_compact", T, Gev, _p(mask), _p(offsets), _p(idx), _stream())
         return CandidateLists(offsets, idx[:nnz], chunk_off, nnz, nchunks, mask)
@@ -318,7 +362,8 @@ class HotPath:
             qrec = torch.empty(B, self.L["qrec"], dtype=torch.float32, device=self.device)
             loss_part = torch.empty(T, dtype=torch.float64, device=self.device)
         self._ev("forward", 0)
-        if self.forward_impl == "tc":
+        self.last_forward_impl = "tc" if self.forward_tc_ok(recs) else "fp32"
+        if self.last_forward_impl == "tc":
             K.call("ndg_forward_tc", self.n, B, self.tile, _p(queries), _p(targets), _p(recs.rec_tc),
                    _p(cl.offsets), _p(cl.idx), self.eps, int(n_total or B), _p(pred), _p(qrec), _p(loss_part), _stream())
         else:
@@ -337,7 +382,8 @@ class HotPath:
         B = int(qrec.shape[0])
         accum = torch.zeros(recs.Gev, self.L["acc"], dtype=torch.float64, device=self.device)
         self._ev("backward", 0)
-        if self.backward_impl == "tc":
+        self.last_backward_impl = "tc" if self.backward_tc_ok(recs) else "fp32"
+        if self.last_backward_impl == "tc":
             K.call("ndg_backward_tc", self.n, B, self.tile, _p(qrec), _p(recs.rec_tc), _p(cl.offsets), _p(cl.idx),
                    _p(accum), _stream())
             self._ev("backward", 1)

@@ -45,7 +45,7 @@ SIGNATURES = {
     "ndg_active_mask": [_I, _L, _I, _P, _P, _P, _P, _L, _D, _P, _P, _P],
     "ndg_epilogue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "ndg_adam": [_I, _L, _P, _P, _P, _P, _P, _I, _F, _F, _F, _F, _F, _F, _F, _P],
-    "ndg_tc_records": [_I, _L, _P, _P, _P, _P, _P, _P],
+    "ndg_tc_records": [_I, _L, _P, _P, _P, _P, _P, _P, _P],
     "ndg_forward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _F, _L, _P, _P, _P, _P],
     "ndg_fp32_probe": [_P, _I, _I, _P],
     "ndg_fp32_probe_flops": [_I, _I],

@@ -263,14 +263,18 @@ def test_adam_matches_oracle(cuda):
     assert np.array_equal(mix.params.cpu().numpy(), p)
 
 
-@pytest.mark.parametrize("sigma0,regime", [(0.15, "R"), (0.05, "C"), (0.02, "C")])
-def test_tc_forward_sharp_gaussians(cuda, sigma0, regime):
+@pytest.mark.parametrize("sigma0,regime,want_tc", [(0.15, "R", True), (0.05, "C", True), (0.02, "C", False),
+                                                    (0.005, "R", False)])
+def test_tc_forward_sharp_gaussians(cuda, sigma0, regime, want_tc):
     """Tensor-core forward (3xTF32 z-GEMM) vs the float64 oracle on sharp Gaussians (the regime where
-    the fp32 cancellation of the centred features is largest, tools/tc_precision_study.py)."""
+    the fp32 cancellation of the centred features is largest, tools/tc_precision_study.py). Past the
+    conditioning bound (HotPath.TC_FORWARD_MAX_BOUND) the step runs the FP32-pipe K5 instead; both
+    sides of the bound must meet the 1e-4 bar."""
     ndg = _ndg()
     om, mix, q, t = _mk(10, 800, 2048, regime=regime, sigma0=sigma0)
     hp = ndg.HotPath(10, projection_seed=2, forward="tc")
     res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    assert hp.last_forward_impl == ("tc" if want_tc else "fp32")
     ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
     assert np.array_equal(res.candidates.idx.cpu().numpy(), ref["idx"])
     assert _rel(res.pred.cpu().numpy(), ref["pred"]) < RTOL

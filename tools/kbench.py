@@ -31,6 +31,6 @@ n = a.n_dims
 pairs = res.candidates.n_pairs_tiles * 256
 f = statistics.median(hp.kernel_ms("forward")); b = statistics.median(hp.kernel_ms("backward"))
 g = res.grads.flat.double()
-print(json.dumps(dict(lib=os.path.basename(os.environ.get("NDG_LIB", "libndg.so")), fwd=hp.forward_impl, regime=a.regime, n=n,
+print(json.dumps(dict(lib=os.path.basename(os.environ.get("NDG_LIB", "libndg.so")), fwd=hp.last_forward_impl, bwd=hp.last_backward_impl, regime=a.regime, n=n,
       fwd_ms=f, bwd_ms=b, fwd_tflops=pairs * (n*n+3*n+8) / f / 1e9, bwd_tflops=pairs * (2*n*n+6*n+14) / b / 1e9,
       kept=res.kept_fraction, loss=res.loss, grad_checksum=float(g.abs().sum()), pred_sum=float(res.pred.double().sum()))))
