@@ -45,6 +45,21 @@ constexpr int kTBuf = NDG_TC_TBUF;            // TMEM accumulator buffers (x 2 q
 
 constexpr int kARing = 8;                     // colour ring depth (independent of the B ring)
 
+#ifdef NDG_TCX_TRACE
+// Timeline probe (tuning builds only): clock64 at each hand-off of the first kTrC chunks of one CTA.
+constexpr int kTrC = 64, kTrEv = 10;
+__device__ long long g_trace[kTrC * kTrEv];
+#define NDG_TR(ev, c)                                                                          \
+    do {                                                                                       \
+        if (blockIdx.x == kTraceCta && (c) < kTrC) g_trace[(c) * kTrEv + (ev)] = clock64();  \
+    } while (0)
+constexpr unsigned kTraceCta = 300;
+#else
+#define NDG_TR(ev, c) \
+    do {              \
+    } while (0)
+#endif
+
 template <int N>
 struct TcCfg {
     static constexpr int K = tc_k(N);
@@ -62,6 +77,7 @@ struct TcCfg {
     // staging depth: as deep as NDG_TC_STAGING, but the whole ring set must fit in shared memory
     static constexpr int STG = (kFixed + kTcStaging * kSlot <= kBudget) ? kTcStaging : (int)((kBudget - kFixed) / kSlot);
     static_assert(STG >= 2, "shared-memory budget too small for the staging ring");
+    static_assert(kARing >= kTcStages + kTBuf + 1, "colour-slot reuse relies on the B-stage wait (splitters)");
 };
 
 template <int N>
@@ -90,7 +106,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     float* sStage = reinterpret_cast<float*>(sB + kTcStages * 2 * P * kPlane);    // [staging][C][RT]
     float* sAval = sStage + STG * C * RT;                                   // [kARing][C][4]
     __shared__ __align__(8) uint64_t sfull[STG], sempty[STG];
-    __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], aempty_bar[kARing];
+    __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages];
     __shared__ __align__(8) uint64_t tfull_bar[kTBuf], tempty_bar[kTBuf];
     __shared__ uint32_t s_tbase;
     __shared__ double s_loss[8];
@@ -110,7 +126,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_init(&full_bar[s], kSplit);
             mbar_init(&empty_bar[s], 1);
         }
-        for (int s = 0; s < kARing; ++s) mbar_init(&aempty_bar[s], kEpiW);
         for (int b = 0; b < kTBuf; ++b) {
             mbar_init(&tfull_bar[b], 1);
             mbar_init(&tempty_bar[b], kEpiW);
@@ -168,6 +183,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) bulk_g2s(sStage + (sl * C) * RT, rec_tc, n_in * RT * 4, &sfull[sl]);
 #else
             if (lane < n_in) bulk_g2s(sStage + (sl * C + lane) * RT, rec_tc + e0 * RT, RT * 4, &sfull[sl]);
+            if (lane == 0) NDG_TR(0, c);
 #endif
             e0 = e1;
             e1 = e2;
@@ -179,7 +195,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int c = 0; c < nchunks; ++c) {
                 const int s = c % kTcStages, b = c % kTBuf;
                 mbar_wait(&full_bar[s], (uint32_t)(c / kTcStages) & 1);
+                NDG_TR(3, c);
                 if (c >= kTBuf) mbar_wait(&tempty_bar[b], (uint32_t)((c / kTBuf) - 1) & 1);
+                NDG_TR(4, c);
                 tc::fence_after();
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -198,6 +216,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 tc::commit(&empty_bar[s]);      // B stage s may be refilled
                 tc::commit(&tfull_bar[b]);      // accumulators of buffer b are ready
+                NDG_TR(5, c);
             }
         }
         __syncwarp();
@@ -221,20 +240,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int sl = c % STG, s = c % kTcStages;
             const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
             mbar_wait(&sfull[sl], (uint32_t)(c / STG) & 1);
+            if (warp == 2 && lane == 0) NDG_TR(1, c);
             const int as = c % kARing;
+            // B stage s free again. This also frees colour slot `as` (last used by chunk c - kARing):
+            // MMA(c - kTcStages) was issued after tempty(c - kTcStages - kTBuf), which every epilogue
+            // warp arrives only after finishing chunk c - kTcStages - kTBuf - 1 >= c - kARing.
             if (c >= kTcStages) mbar_wait(&empty_bar[s], (uint32_t)((c / kTcStages) - 1) & 1);
-            if (c >= kARing) mbar_wait(&aempty_bar[as], (uint32_t)((c / kARing) - 1) & 1);
             const float* stg = sStage + sl * C * RT;
             uint8_t* bhi = sB + (s * 2 + 0) * P * kPlane;
             uint8_t* blo = sB + (s * 2 + 1) * P * kPlane;
 #ifndef NDG_TCX_NOSPLIT
             // records are plane-major ([p][i][4]): consecutive lanes read consecutive 16-B staging
             // units and write consecutive rows of one plane -> both conflict-free
-            const int n_units = n_in * N * P;
-#pragma unroll
-            for (int k = 0; k < KU; ++k) {
-                if (pl + k * NSL >= n_units) break;
-                const float4 v = *reinterpret_cast<const float4*>(stg + src_off[k]);
+            auto split_store = [&](int k, const float4& v) {
                 float4 hi, lo;
                 tc::split_tf32(v.x, hi.x, lo.x);
                 tc::split_tf32(v.y, hi.y, lo.y);
@@ -242,6 +260,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tc::split_tf32(v.w, hi.w, lo.w);
                 *reinterpret_cast<float4*>(bhi + dst_off[k]) = hi;
                 *reinterpret_cast<float4*>(blo + dst_off[k]) = lo;
+            };
+            if (n_in == C) {      // full chunk: all loads in flight before the first split
+                constexpr int kLast = C * N * P - (KU - 1) * NSL;   // threads active in the last round
+                float4 v[KU];
+#pragma unroll
+                for (int k = 0; k < KU; ++k)
+                    if (k < KU - 1 || pl < kLast) v[k] = *reinterpret_cast<const float4*>(stg + src_off[k]);
+#pragma unroll
+                for (int k = 0; k < KU; ++k)
+                    if (k < KU - 1 || pl < kLast) split_store(k, v[k]);
+            } else {
+                const int n_units = n_in * N * P;
+#pragma unroll
+                for (int k = 0; k < KU; ++k) {
+                    if (pl + k * NSL >= n_units) break;
+                    split_store(k, *reinterpret_cast<const float4*>(stg + src_off[k]));
+                }
             }
 #endif
             for (int u = pl; u < n_in; u += NSL)
@@ -251,6 +286,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&full_bar[s]);
+                if (warp == 2) NDG_TR(2, c);
                 mbar_arrive(&sempty[sl]);
             }
         }
@@ -266,6 +302,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int as = c % kARing, b = c % kTBuf;
             const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
             mbar_wait(&tfull_bar[b], (uint32_t)(c / kTBuf) & 1);
+            if (warp == kEpi0 && lane == 0) NDG_TR(6, c);
             tc::fence_after();
             float v[NLD * 16];
             const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((b * 2 + h) * kNCol + grp * CG * N);
@@ -279,6 +316,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty_bar[b]);      // TMEM buffer b may be overwritten
+            if (warp == kEpi0 && lane == 0) NDG_TR(7, c);
 #ifndef NDG_TCX_NOEPI
             auto gauss = [&](int gl) {
                 const int g = grp * CG + gl;
@@ -317,8 +355,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #else
             pp[0] += v[0] + v[NLD * 16 - 1];
 #endif
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&aempty_bar[as]);
+            if (warp == kEpi0 && lane == 0) NDG_TR(8, c);
+            if (warp == kEpi0 + 7 && lane == 0) NDG_TR(9, c);
         }
         // tile end: pred, rel-L2 loss, backward query record of this thread's query
         double loss_acc = 0.0;
@@ -449,6 +487,12 @@ __global__ void tc_records_kernel(int n, int64_t Gev, const double* __restrict__
 }
 
 }  // namespace
+
+#ifdef NDG_TCX_TRACE
+extern "C" int ndg_trace_dump(long long* out) {
+    return cudaMemcpyFromSymbol(out, g_trace, sizeof(long long) * kTrC * kTrEv) == cudaSuccess ? 0 : -3;
+}
+#endif
 
 extern "C" int ndg_tc_records(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
                               const float* rec, float* rec_tc, double* cond, void* stream) {
