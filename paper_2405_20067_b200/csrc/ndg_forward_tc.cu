@@ -33,7 +33,14 @@ constexpr int kSplit = NDG_TC_SPLITTERS;   // splitter warps (2 .. 2 + kSplit - 
 constexpr int kEpiG = NDG_TC_EPIG;          // epilogue warps per (query half, lane quarter)
 constexpr int kEpi0 = 2 + kSplit;           // first epilogue warp (a multiple of 4: lane quarter = warp % 4)
 constexpr int kEpiW = 8 * kEpiG;            // epilogue warps
-constexpr int kTcWarps = kEpi0 + kEpiW;
+#ifndef NDG_TC_PRODUCERS
+#define NDG_TC_PRODUCERS 2
+#endif
+// Producer warps: warp 0 and (with 2) the last warp. A cp.async.bulk gather issues through the uniform
+// datapath one record at a time, so one warp issuing all of a chunk's records paced the pipeline
+// (tools/tc_trace.py: half the gathers -> -10%); producer p takes chunks c = p (mod kProd).
+constexpr int kProd = NDG_TC_PRODUCERS;
+constexpr int kTcWarps = kEpi0 + kEpiW + (kProd - 1);
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcStages = 4;         // B-operand / colour ring
 constexpr int kTcStaging = NDG_TC_STAGING;   // raw-record staging ring depth (capped per N by the smem budget)
@@ -162,7 +169,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc::fence_after();
     const uint32_t tbase = s_tbase;
 
-    if (warp == 0) {
+    if (warp == 0 || (kProd > 1 && warp == kTcWarps - 1)) {
         // ------------------------------ TMA producer -------------------------------------------
         // lane g < C owns candidate g of every chunk; its index is loaded two chunks ahead so the
         // dependent idx -> record address load never sits on the chunk's critical path.
@@ -170,19 +177,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int64_t pos = beg + (int64_t)c * C + lane;
             return (lane < C && c < nchunks && pos < end) ? (int64_t)__ldg(idx + pos) : 0;
         };
-        int64_t e0 = load_idx(0), e1 = load_idx(1);
-        for (int c = 0; c < nchunks; ++c) {
-            const int64_t e2 = load_idx(c + 2);
+        const int pid = warp == 0 ? 0 : 1;
+        int64_t e0 = load_idx(pid), e1 = load_idx(pid + kProd);
+        for (int c = pid; c < nchunks; c += kProd) {
+            const int64_t e2 = load_idx(c + 2 * kProd);
             const int sl = c % STG;
             if (c >= STG) mbar_wait(&sempty[sl], (uint32_t)((c / STG) - 1) & 1);
             const int64_t cb = beg + (int64_t)c * C;
             const int n_in = (int)imin64(C, end - cb);
-            if (lane == 0) mbar_arrive_expect_tx(&sfull[sl], (uint32_t)(n_in * RT * 4));
+#ifdef NDG_TCX_HALFCOPY
+            const int n_cp = min(n_in, C / 2);     // knock-out: half the gathers (wrong results)
+#else
+            const int n_cp = n_in;
+#endif
+            if (lane == 0) mbar_arrive_expect_tx(&sfull[sl], (uint32_t)(n_cp * RT * 4));
             __syncwarp();
 #ifdef NDG_TCX_ONECOPY
             if (lane == 0) bulk_g2s(sStage + (sl * C) * RT, rec_tc, n_in * RT * 4, &sfull[sl]);
 #else
-            if (lane < n_in) bulk_g2s(sStage + (sl * C + lane) * RT, rec_tc + e0 * RT, RT * 4, &sfull[sl]);
+            if (lane < n_cp) bulk_g2s(sStage + (sl * C + lane) * RT, rec_tc + e0 * RT, RT * 4, &sfull[sl]);
             if (lane == 0) NDG_TR(0, c);
 #endif
             e0 = e1;
