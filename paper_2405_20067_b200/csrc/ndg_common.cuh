@@ -10,7 +10,10 @@
 namespace ndg {
 
 constexpr int NMAX = 16;
-constexpr int kBwdChunk = 128;          // candidates per backward work item (one per thread)
+#ifndef NDG_BWD_CHUNK
+#define NDG_BWD_CHUNK 128
+#endif
+constexpr int kBwdChunk = NDG_BWD_CHUNK;  // candidates per backward work item (one per thread)
 constexpr int kNumStats = 3;
 
 __host__ __device__ constexpr int n_chol(int n) { return n * (n + 1) / 2; }
