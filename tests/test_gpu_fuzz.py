@@ -1,7 +1,10 @@
 """Seeded random sweep of the whole hot path against the float64 oracle: dimension, mixture size,
 tile size (including non-powers of two, tiles smaller than one 128-query MMA half and tiles larger
 than the tensor-core forward's 256), children, amplitude mode, query regime and both implementations
-of K5 and K7. Same bars as test_gpu_parity.py (CSR bit-exact, 1e-4 block-relative)."""
+of K5 and K7. Same bars as test_gpu_parity.py (CSR bit-exact, 1e-4 block-relative).
+NDG_FUZZ_CASES / NDG_FUZZ_SEED widen the sweep (default 24 cases)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -12,7 +15,7 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-4
 
 
-def _cases(n_cases=24, seed=20261018):
+def _cases(n_cases=int(os.environ.get("NDG_FUZZ_CASES", "24")), seed=int(os.environ.get("NDG_FUZZ_SEED", "20261018"))):
     rng = np.random.default_rng(seed)
     out = []
     for i in range(n_cases):
