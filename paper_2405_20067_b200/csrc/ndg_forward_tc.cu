@@ -27,12 +27,9 @@ namespace {
 #define NDG_TC_STAGING 8
 #endif
 constexpr int kSplit = NDG_TC_SPLITTERS;   // splitter warps (2 .. 2 + kSplit - 1)
-#ifndef NDG_TC_EPIG
-#define NDG_TC_EPIG 1
-#endif
-constexpr int kEpiG = NDG_TC_EPIG;          // epilogue warps per (query half, lane quarter)
 constexpr int kEpi0 = 2 + kSplit;           // first epilogue warp (a multiple of 4: lane quarter = warp % 4)
-constexpr int kEpiW = 8 * kEpiG;            // epilogue warps
+constexpr int kEpiW = 8;                    // epilogue warps (2 query halves x 4 lane quarters)
+static_assert(kEpi0 % 4 == 0, "epilogue warp w must own TMEM lane quarter w % 4");
 #ifndef NDG_TC_PRODUCERS
 #define NDG_TC_PRODUCERS 2
 #endif
@@ -117,7 +114,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __shared__ __align__(8) uint64_t tfull_bar[kTBuf], tempty_bar[kTBuf];
     __shared__ uint32_t s_tbase;
     __shared__ double s_loss[8];
-    __shared__ float s_pp[kEpiG > 1 ? 256 * 3 : 1];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t t = blockIdx.x;
@@ -305,11 +301,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else {
         // ------------------------------ epilogue -----------------------------------------------
-        const int h = ((warp - kEpi0) >> 2) & 1, q4 = warp & 3, grp = (warp - kEpi0) >> 3;
-        // Gaussians [grp * CG, grp * CG + CG) of every chunk: kEpiG warps share a lane quarter so more
-        // warps keep TMEM reads in flight (TMEM read throughput scales with the number of loading warps)
-        constexpr int CG = (C + kEpiG - 1) / kEpiG;
-        constexpr int NLD = (CG * N + 15) / 16;
+        const int h = (warp - kEpi0) >> 2, q4 = warp & 3;
+        constexpr int NLD = (C * N + 15) / 16;
         float pp[3] = {0.f, 0.f, 0.f};
         for (int c = 0; c < nchunks; ++c) {
             const int as = c % kARing, b = c % kTBuf;
@@ -318,7 +311,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (warp == kEpi0 && lane == 0) NDG_TR(6, c);
             tc::fence_after();
             float v[NLD * 16];
-            const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((b * 2 + h) * kNCol + grp * CG * N);
+            const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((b * 2 + h) * kNCol);
 #ifdef NDG_TCX_NOLD
             for (int j = 0; j < NLD * 16; ++j) v[j] = (float)(ta + j);
 #else
@@ -331,22 +324,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) mbar_arrive(&tempty_bar[b]);      // TMEM buffer b may be overwritten
             if (warp == kEpi0 && lane == 0) NDG_TR(7, c);
 #ifndef NDG_TCX_NOEPI
-            auto gauss = [&](int gl) {
-                const int g = grp * CG + gl;
+            auto gauss = [&](int g) {
                 {
                     float sum;
                     if constexpr ((N & 1) == 0) {
                         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
                         for (int i = 0; i < N; i += 2) {
-                            const float2 zz = make_float2(v[gl * N + i], v[gl * N + i + 1]);
+                            const float2 zz = make_float2(v[g * N + i], v[g * N + i + 1]);
                             acc = __ffma2_rn(zz, zz, acc);
                         }
                         sum = acc.x + acc.y;
                     } else {
                         sum = 0.f;
 #pragma unroll
-                        for (int i = 0; i < N; ++i) sum = fmaf(v[gl * N + i], v[gl * N + i], sum);
+                        for (int i = 0; i < N; ++i) sum = fmaf(v[g * N + i], v[g * N + i], sum);
                     }
                     const float gv = ex2_neg(sum);
                     const float4 av = *reinterpret_cast<const float4*>(sAval + (as * C + g) * 4);
@@ -355,15 +347,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     pp[2] = fmaf(gv, av.z, pp[2]);
                 }
             };
-            if (n_in == C && (kEpiG == 1 || C % kEpiG == 0)) {   // full chunk: no per-Gaussian predicates
+            if (n_in == C) {      // full chunk: no per-Gaussian predicates
 #pragma unroll
-                for (int gl = 0; gl < CG; ++gl) gauss(gl);
+                for (int g = 0; g < C; ++g) gauss(g);
             } else {
 #pragma unroll
-                for (int gl = 0; gl < CG; ++gl) {
-                    const int g = grp * CG + gl;
-                    if (g < n_in && g < C) gauss(gl);
-                }
+                for (int g = 0; g < C; ++g)
+                    if (g < n_in) gauss(g);
             }
 #else
             pp[0] += v[0] + v[NLD * 16 - 1];
@@ -374,20 +364,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // tile end: pred, rel-L2 loss, backward query record of this thread's query
         double loss_acc = 0.0;
         const int qi = h * 128 + q4 * 32 + lane;
-        if constexpr (kEpiG > 1) {   // fold the other groups' partial predictions into group 0
-            if (grp > 0) {
-                s_pp[qi * 3] = pp[0];
-                s_pp[qi * 3 + 1] = pp[1];
-                s_pp[qi * 3 + 2] = pp[2];
-            }
-            asm volatile("bar.sync 1, %0;" ::"r"(kEpiW * 32) : "memory");
-        }
-        if ((kEpiG == 1 || grp == 0) && qi < tile) {
-            if constexpr (kEpiG > 1) {
-                pp[0] += s_pp[qi * 3];
-                pp[1] += s_pp[qi * 3 + 1];
-                pp[2] += s_pp[qi * 3 + 2];
-            }
+        if (qi < tile) {
             const int64_t bq = t * tile + qi;
             pred[bq * 3] = pp[0];
             pred[bq * 3 + 1] = pp[1];
@@ -410,7 +387,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 loss_acc = ell;
             }
         }
-        if (targets && (kEpiG == 1 || grp == 0)) {
+        if (targets) {
 #pragma unroll
             for (int o = 16; o; o >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
             if (lane == 0) s_loss[warp - kEpi0] = loss_acc;
