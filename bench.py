@@ -56,8 +56,15 @@ def parse():
     return ap.parse_args()
 
 
+def config_label(a) -> str:
+    """BASELINE.json config this workload matches (configs[i] -> "cfg{i+1}"), else "custom"."""
+    table = {(6, 4096, 16384): "cfg1", (10, 100_000, 1 << 20): "cfg2", (16, 500_000, 1 << 22): "cfg4",
+             (10, 1_000_000, 1 << 19): "cfg5 (per-GPU shard of 2^22 at 8 GPUs)"}
+    return table.get((a.n_dims, a.gaussians, a.batch), "custom")
+
+
 def workload_name(a, regime):
-    return (f"cfg2: {a.n_dims}-D synthetic shading-shaped mixture, {a.gaussians} Gaussians"
+    return (f"{config_label(a)}: {a.n_dims}-D synthetic shading-shaped mixture, {a.gaussians} Gaussians"
             f"{' (+live children)' if a.children else ''}, {a.batch} queries/GPU/step, tile {a.tile}, "
             f"k={a.k}, multiplier 3, regime {regime} "
             f"({'U[0,1)^N sorted by dim 0' if regime == 'R' else 'coherent tiles, spread 0.01'})")
