@@ -251,14 +251,18 @@ extern "C" int ndg_tile_bounds(int n, int64_t B, int tile, const float* queries,
 
 // ---------------------------------------------------------------------------------------------
 // K4a cull mask: cull_tile for all tiles. Thread = evaluated Gaussian, CTA =
-// 256 Gaussians x kCullTiles tiles; the Gaussians' (m_r, thr) sit in shared memory, the tiles'
-// intervals are broadcast. Culled iff any vector has lo - m_r > thr or m_r - hi > thr (FP64; the
-// same predicate as max(lo - m_r, m_r - hi, 0) > multiplier * s_r); thr < 0 = never evaluated.
-// Warp ballot -> one mask word per 32 Gaussians; per-CTA popcount -> one atomic per tile.
+// 256 Gaussians x TILES tiles; the tiles' intervals sit in shared memory and are broadcast, the
+// Gaussian's (m_r, thr) live in registers for k <= 16 (shared memory otherwise). Culled iff any
+// vector has lo - m_r > thr or m_r - hi > thr (FP64; the same predicate as
+// max(lo - m_r, m_r - hi, 0) > multiplier * s_r); thr < 0 = never evaluated. Warp ballot -> one mask
+// word per 32 Gaussians; per-CTA popcount -> one atomic per tile.
 // ---------------------------------------------------------------------------------------------
 constexpr int kCullThreads = 256;
-constexpr int kCullTiles = 16;
+constexpr int kCullRegK = 16;          // k handled from registers
+constexpr int kCullTilesReg = 64;      // tiles per CTA on the register path (amortises the (m_r, thr) loads)
+constexpr int kCullTilesSmem = 16;
 
+template <bool REG>
 __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int k, int64_t Gev,
                                                                   const double* __restrict__ lo,
                                                                   const double* __restrict__ hi,
@@ -266,33 +270,66 @@ __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int 
                                                                   const double* __restrict__ thr,
                                                                   uint32_t* __restrict__ mask,
                                                                   int64_t* __restrict__ counts) {
+    constexpr int TILES = REG ? kCullTilesReg : kCullTilesSmem;
     extern __shared__ double sm[];
-    double* s_m = sm;                              // [k][256]
-    double* s_t = sm + k * kCullThreads;           // [k][256]
-    double* s_lo = s_t + k * kCullThreads;         // [kCullTiles][k]
-    double* s_hi = s_lo + kCullTiles * k;
-    __shared__ int s_cnt[kCullTiles][kCullThreads / 32];
+    double* s_lo = sm;                             // [TILES][k]
+    double* s_hi = s_lo + TILES * k;
+    double* s_m = s_hi + TILES * k;                // [k][256] (shared-memory path only)
+    double* s_t = s_m + k * kCullThreads;
+    __shared__ int s_cnt[TILES][kCullThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t e = blockIdx.x * (int64_t)kCullThreads + tid;
-    const int64_t t0 = blockIdx.y * (int64_t)kCullTiles;
-    const int ntile = (int)imin64(kCullTiles, T - t0);
-    for (int ri = 0; ri < k; ++ri) {
-        s_m[ri * kCullThreads + tid] = e < Gev ? m_r[ri * Gev + e] : 0.0;
-        s_t[ri * kCullThreads + tid] = e < Gev ? thr[ri * Gev + e] : -1.0;
-    }
+    const int64_t t0 = blockIdx.y * (int64_t)TILES;
+    const int ntile = (int)imin64(TILES, T - t0);
     for (int x = tid; x < ntile * k; x += kCullThreads) {
         s_lo[x] = lo[t0 * k + x];
         s_hi[x] = hi[t0 * k + x];
     }
+    double mr_r[kCullRegK], th_r[kCullRegK];
+    bool never;
+    if constexpr (REG) {
+#pragma unroll
+        for (int ri = 0; ri < kCullRegK; ++ri) {
+            mr_r[ri] = (ri < k && e < Gev) ? m_r[ri * Gev + e] : 0.0;
+            th_r[ri] = (ri < k && e < Gev) ? thr[ri * Gev + e] : -1.0;
+        }
+        never = th_r[0] < 0.0;
+    } else {
+        for (int ri = 0; ri < k; ++ri) {
+            s_m[ri * kCullThreads + tid] = e < Gev ? m_r[ri * Gev + e] : 0.0;
+            s_t[ri * kCullThreads + tid] = e < Gev ? thr[ri * Gev + e] : -1.0;
+        }
+        never = (e < Gev ? thr[e] : -1.0) < 0.0;
+    }
     __syncthreads();
-    const bool never = s_t[tid] < 0.0;
     const int64_t W = (Gev + 31) / 32;
     for (int tt = 0; tt < ntile; ++tt) {
         bool kept = !never;
-        for (int ri = 0; ri < k && kept; ++ri) {
-            const double mr = s_m[ri * kCullThreads + tid], th = s_t[ri * kCullThreads + tid];
-            const double l = s_lo[tt * k + ri], h = s_hi[tt * k + ri];
-            if (__dsub_rn(l, mr) > th || __dsub_rn(mr, h) > th) kept = false;
+        if constexpr (REG) {
+#ifdef NDG_CULL_EARLY_EXIT
+#pragma unroll
+            for (int ri = 0; ri < kCullRegK; ++ri) {
+                if (ri < k && kept) {
+                    const double l = s_lo[tt * k + ri], h = s_hi[tt * k + ri];
+                    if (__dsub_rn(l, mr_r[ri]) > th_r[ri] || __dsub_rn(mr_r[ri], h) > th_r[ri]) kept = false;
+                }
+            }
+#else
+            // all k tests, branch-free: independent FP64 chains instead of a serial test-and-branch
+#pragma unroll
+            for (int ri = 0; ri < kCullRegK; ++ri) {
+                if (ri < k) {
+                    const double l = s_lo[tt * k + ri], h = s_hi[tt * k + ri];
+                    kept &= !(__dsub_rn(l, mr_r[ri]) > th_r[ri]) & !(__dsub_rn(mr_r[ri], h) > th_r[ri]);
+                }
+            }
+#endif
+        } else {
+            for (int ri = 0; ri < k && kept; ++ri) {
+                const double mr = s_m[ri * kCullThreads + tid], th = s_t[ri * kCullThreads + tid];
+                const double l = s_lo[tt * k + ri], h = s_hi[tt * k + ri];
+                if (__dsub_rn(l, mr) > th || __dsub_rn(mr, h) > th) kept = false;
+            }
         }
         const uint32_t word = __ballot_sync(0xffffffffu, kept);
         if (lane == 0) {
@@ -313,15 +350,21 @@ extern "C" int ndg_cull_mask(int64_t T, int k, int64_t Gev, const double* lo, co
                              const double* thr, uint32_t* mask, int64_t* counts, void* stream) {
     NDG_REQUIRE(k >= 1 && k <= 64, "k must be in 1..64 for the cull kernel");
     if (T == 0 || Gev == 0) return NDG_OK;
-    dim3 grid((unsigned)((Gev + kCullThreads - 1) / kCullThreads), (unsigned)((T + kCullTiles - 1) / kCullTiles));
+    const bool reg = k <= kCullRegK;
+    const int tiles = reg ? kCullTilesReg : kCullTilesSmem;
+    dim3 grid((unsigned)((Gev + kCullThreads - 1) / kCullThreads), (unsigned)((T + tiles - 1) / tiles));
     NDG_REQUIRE(grid.y <= 65535, "too many tiles for one cull launch");
-    size_t smem = sizeof(double) * (2 * k * kCullThreads + 2 * kCullTiles * k);
+    const size_t smem = sizeof(double) * (2 * tiles * k + (reg ? 0 : 2 * k * kCullThreads));
     static thread_local bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(cull_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(cull_mask_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(cull_mask_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         attr_set = true;
     }
-    cull_mask_kernel<<<grid, kCullThreads, smem, as_stream(stream)>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts);
+    if (reg)
+        cull_mask_kernel<true><<<grid, kCullThreads, smem, as_stream(stream)>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts);
+    else
+        cull_mask_kernel<false><<<grid, kCullThreads, smem, as_stream(stream)>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }
@@ -406,11 +449,15 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(int64_t Gev, c
             if (w < warp) before += s_warp[w];
             total += s_warp[w];
         }
-        int64_t pos = s_base + before + incl - c;
-        while (word) {
-            int b = __ffs(word) - 1;
-            idx[pos++] = (int32_t)(wi * 32 + b);
-            word &= word - 1;
+        const int64_t pos = s_base + before + incl - c;
+        // warp-cooperative expansion: word `src` of the warp is written by all lanes (lane l writes the
+        // index of bit l), so dense words become one coalesced 128-B store instead of 32 strided ones
+        for (int src = 0; src < 32; ++src) {
+            const uint32_t wd = __shfl_sync(0xffffffffu, word, src);
+            if (wd == 0u) continue;                               // warp-uniform
+            const int64_t p = __shfl_sync(0xffffffffu, pos, src);
+            if ((wd >> lane) & 1u)
+                idx[p + __popc(wd & ((1u << lane) - 1u))] = (int32_t)((w0 + warp * 32 + src) * 32 + lane);
         }
         __syncthreads();
         if (tid == 0) s_base += total;
