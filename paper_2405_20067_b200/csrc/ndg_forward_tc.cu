@@ -39,9 +39,7 @@ static_assert(kEpi0 % 4 == 0, "epilogue warp w must own TMEM lane quarter w % 4"
 constexpr int kProd = NDG_TC_PRODUCERS;
 constexpr int kTcWarps = kEpi0 + kEpiW + (kProd - 1);
 constexpr int kTcThreads = kTcWarps * 32;
-constexpr int kTcStages = 4;         // B-operand / colour ring
 constexpr int kTcStaging = NDG_TC_STAGING;   // raw-record staging ring depth (capped per N by the smem budget)
-constexpr int kPlane = 128 * 16;     // bytes per operand plane (128 rows x 16 B)
 #ifndef NDG_TC_TBUF
 #define NDG_TC_TBUF 2
 #endif
@@ -64,24 +62,47 @@ constexpr unsigned kTraceCta = 300;
     } while (0)
 #endif
 
+#ifndef NDG_TC_ITEMS
+#define NDG_TC_ITEMS 1
+#endif
+// Items mode: a chunk's MMA covers twice the Gaussians (N = 224 at N = 10) and one query half at a time
+// (item = (chunk, half) -> TMEM buffer = half), so each tcgen05.mma does twice the work per issue; the
+// epilogue splits a chunk's Gaussians into two groups per lane quarter (columns [0, CG*N) and
+// [GOFF, GOFF + (C-CG)*N), GOFF 16-aligned).
+constexpr bool kItems = NDG_TC_ITEMS;
+
 template <int N>
 struct TcCfg {
     static constexpr int K = tc_k(N);
     static constexpr int P = K / 4;
     static constexpr int KS = K / 8;
     // TMEM: A operand (2 halves x hi/lo x K columns) + kTBuf buffers x 2 halves x NCOL accumulator columns
+    // (items: kTBuf buffers x NCOL, one per query half)
     static constexpr int ACOLS = 4 * K;
-    static constexpr int NCOL = ((512 - ACOLS) / (2 * kTBuf)) & ~15;     // MMA N (112 at N = 10)
-    static constexpr int A0 = 2 * kTBuf * NCOL;                          // first A column
-    static constexpr int C = (NCOL / N < 32 ? NCOL / N : 32);
+    static constexpr int NCOL = kItems ? ((512 - ACOLS) / kTBuf) & ~15 : ((512 - ACOLS) / (2 * kTBuf)) & ~15;
+    static constexpr int A0 = kItems ? kTBuf * NCOL : 2 * kTBuf * NCOL;   // first A column
+    static constexpr int ROWS = kItems ? NCOL : 128;                      // B operand rows per plane
+    static constexpr int PLANE = ROWS * 16;
+    static constexpr int items_c() {
+        int c = NCOL / N < 32 ? NCOL / N : 32;
+        while (c > 1 && ((((c + 1) / 2) * N + 15) / 16) * 16 + (c - (c + 1) / 2) * N > NCOL) --c;
+        return c;
+    }
+    static constexpr int C = kItems ? items_c() : (NCOL / N < 32 ? NCOL / N : 32);
+    static constexpr int CG = kItems ? (C + 1) / 2 : C;                   // Gaussians of epilogue group 0
+    static constexpr int GOFF = kItems ? ((CG * N + 15) / 16) * 16 : 0;   // first column of group 1
     static constexpr int RT = tc_rec_floats(N);       // floats per raw record (rows | a | pad)
-    static constexpr size_t kFixed = (size_t)(kTcStages * 2) * P * kPlane + (size_t)kARing * C * 16;
+    static constexpr size_t kRing = (size_t)kARing * C * 16;
     static constexpr size_t kSlot = (size_t)C * RT * 4;
-    static constexpr size_t kBudget = 225 * 1024;
+    static constexpr size_t kBudget = 222 * 1024;    // 227 KB per CTA minus static shared memory (s_pp, barriers)
+    static constexpr size_t stage_bytes = (size_t)2 * P * PLANE;
+    static constexpr int STAGES = (4 * stage_bytes + kRing + 2 * kSlot <= kBudget) ? 4 : 3;
+    static constexpr size_t kFixed = (size_t)STAGES * stage_bytes + kRing;
     // staging depth: as deep as NDG_TC_STAGING, but the whole ring set must fit in shared memory
     static constexpr int STG = (kFixed + kTcStaging * kSlot <= kBudget) ? kTcStaging : (int)((kBudget - kFixed) / kSlot);
     static_assert(STG >= 2, "shared-memory budget too small for the staging ring");
-    static_assert(kARing >= kTcStages + kTBuf + 1, "colour-slot reuse relies on the B-stage wait (splitters)");
+    static_assert(kARing >= STAGES + kTBuf + 1, "colour-slot reuse relies on the B-stage wait (splitters)");
+    static_assert(!kItems || kTBuf == 2, "items mode keeps one TMEM buffer per query half");
 };
 
 template <int N>
@@ -102,6 +123,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     using Cfg = TcCfg<N>;
     constexpr int K = Cfg::K, P = Cfg::P, KS = Cfg::KS, C = Cfg::C, RT = Cfg::RT, STG = Cfg::STG;
     constexpr int kNCol = Cfg::NCOL, kA0 = Cfg::A0;
+    constexpr int kTcStages = Cfg::STAGES, kPlane = Cfg::PLANE, CG = Cfg::CG, GOFF = Cfg::GOFF;
     constexpr int QS = qrec_floats(N);
     constexpr uint32_t IDESC = tc::idesc_tf32(128, kNCol);
 
@@ -114,6 +136,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __shared__ __align__(8) uint64_t tfull_bar[kTBuf], tempty_bar[kTBuf];
     __shared__ uint32_t s_tbase;
     __shared__ double s_loss[8];
+    __shared__ float s_pp[kItems ? 256 * 3 : 1];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t t = blockIdx.x;
@@ -205,12 +228,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const int s = c % kTcStages, b = c % kTBuf;
                 mbar_wait(&full_bar[s], (uint32_t)(c / kTcStages) & 1);
                 NDG_TR(3, c);
-                if (c >= kTBuf) mbar_wait(&tempty_bar[b], (uint32_t)((c / kTBuf) - 1) & 1);
+                if constexpr (!kItems) {
+                    if (c >= kTBuf) mbar_wait(&tempty_bar[b], (uint32_t)((c / kTBuf) - 1) & 1);
+                }
                 NDG_TR(4, c);
                 tc::fence_after();
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const uint32_t d = tbase + (uint32_t)((b * 2 + h) * kNCol);
+                    uint32_t d;
+                    if constexpr (kItems) {          // item (c, h) -> TMEM buffer h
+                        if (c >= 1) mbar_wait(&tempty_bar[h], (uint32_t)(c - 1) & 1);
+                        tc::fence_after();
+                        d = tbase + (uint32_t)(h * kNCol);
+                    } else {
+                        d = tbase + (uint32_t)((b * 2 + h) * kNCol);
+                    }
                     const uint32_t ahi = tbase + (uint32_t)(kA0 + h * 2 * K), alo = ahi + K;
 #pragma unroll
                     for (int ks = 0; ks < KS; ++ks) {
@@ -222,9 +254,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         tc::mma_tf32_ta(d, alo + 8 * ks, bhi, IDESC, 1u);
 #endif
                     }
+                    if constexpr (kItems) tc::commit(&tfull_bar[h]);   // item (c, h) is ready
                 }
                 tc::commit(&empty_bar[s]);      // B stage s may be refilled
-                tc::commit(&tfull_bar[b]);      // accumulators of buffer b are ready
+                if constexpr (!kItems) tc::commit(&tfull_bar[b]);      // accumulators of buffer b are ready
                 NDG_TR(5, c);
             }
         }
@@ -243,7 +276,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int g = u / (N * P), rem = u - g * (N * P);
             const int p = rem / N, i = rem - p * N;
             src_off[k] = g * RT + rem * 4;
-            dst_off[k] = p * kPlane + (g * N + i) * 16;
+            const int row = (kItems && g >= CG) ? GOFF + (g - CG) * N + i : g * N + i;   // D column of (g, i)
+            dst_off[k] = p * kPlane + row * 16;
         }
         for (int c = 0; c < nchunks; ++c) {
             const int sl = c % STG, s = c % kTcStages;
@@ -301,90 +335,117 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else {
         // ------------------------------ epilogue -----------------------------------------------
-        const int h = (warp - kEpi0) >> 2, q4 = warp & 3;
-        constexpr int NLD = (C * N + 15) / 16;
-        float pp[3] = {0.f, 0.f, 0.f};
+        // warp (wh, q4): TMEM lane quarter q4. Default: wh = query half, all C Gaussians of a chunk.
+        // Items: wh = Gaussian group, for both halves' items; pp[hh] is the partial prediction of the
+        // thread's query in half hh (group 1 hands its partials to group 0 at tile end).
+        const int wh = (warp - kEpi0) >> 2, q4 = warp & 3;
+        constexpr int NGW = kItems ? CG : C;            // Gaussian slots per warp per item
+        constexpr int NLD = (NGW * N + 15) / 16;
+        constexpr int NIT = kItems ? 2 : 1;             // items per chunk
+        float pp[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+        const int g0 = kItems ? wh * CG : 0;
+        const int ngw = kItems ? (wh ? C - CG : CG) : C;
         for (int c = 0; c < nchunks; ++c) {
-            const int as = c % kARing, b = c % kTBuf;
+            const int as = c % kARing;
             const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
-            mbar_wait(&tfull_bar[b], (uint32_t)(c / kTBuf) & 1);
-            if (warp == kEpi0 && lane == 0) NDG_TR(6, c);
-            tc::fence_after();
-            float v[NLD * 16];
-            const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((b * 2 + h) * kNCol);
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) {
+                const int b = kItems ? it : c % kTBuf;
+                mbar_wait(&tfull_bar[b], kItems ? (uint32_t)c & 1 : (uint32_t)(c / kTBuf) & 1);
+                if (warp == kEpi0 && lane == 0 && it == 0) NDG_TR(6, c);
+                tc::fence_after();
+                float v[NLD * 16];
+                const uint32_t col = kItems ? (uint32_t)(it * kNCol + wh * GOFF) : (uint32_t)((b * 2 + wh) * kNCol);
+                const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + col;
 #ifdef NDG_TCX_NOLD
-            for (int j = 0; j < NLD * 16; ++j) v[j] = (float)(ta + j);
+                for (int j = 0; j < NLD * 16; ++j) v[j] = (float)(ta + j);
 #else
 #pragma unroll
-            for (int j = 0; j < NLD; ++j) tc::ld16(ta + 16 * j, v + 16 * j);
-            tc::wait_ld();
+                for (int j = 0; j < NLD; ++j) tc::ld16(ta + 16 * j, v + 16 * j);
+                tc::wait_ld();
 #endif
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[b]);      // TMEM buffer b may be overwritten
-            if (warp == kEpi0 && lane == 0) NDG_TR(7, c);
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty_bar[b]);      // TMEM buffer b may be overwritten
+                if (warp == kEpi0 && lane == 0 && it == 0) NDG_TR(7, c);
 #ifndef NDG_TCX_NOEPI
-            auto gauss = [&](int g) {
-                {
+                auto gauss = [&](int gl) {
                     float sum;
                     if constexpr ((N & 1) == 0) {
                         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
                         for (int i = 0; i < N; i += 2) {
-                            const float2 zz = make_float2(v[g * N + i], v[g * N + i + 1]);
+                            const float2 zz = make_float2(v[gl * N + i], v[gl * N + i + 1]);
                             acc = __ffma2_rn(zz, zz, acc);
                         }
                         sum = acc.x + acc.y;
                     } else {
                         sum = 0.f;
 #pragma unroll
-                        for (int i = 0; i < N; ++i) sum = fmaf(v[g * N + i], v[g * N + i], sum);
+                        for (int i = 0; i < N; ++i) sum = fmaf(v[gl * N + i], v[gl * N + i], sum);
                     }
                     const float gv = ex2_neg(sum);
-                    const float4 av = *reinterpret_cast<const float4*>(sAval + (as * C + g) * 4);
-                    pp[0] = fmaf(gv, av.x, pp[0]);
-                    pp[1] = fmaf(gv, av.y, pp[1]);
-                    pp[2] = fmaf(gv, av.z, pp[2]);
+                    const float4 av = *reinterpret_cast<const float4*>(sAval + (as * C + g0 + gl) * 4);
+                    pp[it][0] = fmaf(gv, av.x, pp[it][0]);
+                    pp[it][1] = fmaf(gv, av.y, pp[it][1]);
+                    pp[it][2] = fmaf(gv, av.z, pp[it][2]);
+                };
+                if (n_in == C && (!kItems || C == 2 * CG)) {      // full chunk: no per-Gaussian predicates
+#pragma unroll
+                    for (int gl = 0; gl < NGW; ++gl) gauss(gl);
+                } else {
+#pragma unroll
+                    for (int gl = 0; gl < NGW; ++gl)
+                        if (gl < ngw && g0 + gl < n_in) gauss(gl);
                 }
-            };
-            if (n_in == C) {      // full chunk: no per-Gaussian predicates
-#pragma unroll
-                for (int g = 0; g < C; ++g) gauss(g);
-            } else {
-#pragma unroll
-                for (int g = 0; g < C; ++g)
-                    if (g < n_in) gauss(g);
-            }
 #else
-            pp[0] += v[0] + v[NLD * 16 - 1];
+                pp[it][0] += v[0] + v[NLD * 16 - 1];
 #endif
+            }
             if (warp == kEpi0 && lane == 0) NDG_TR(8, c);
             if (warp == kEpi0 + 7 && lane == 0) NDG_TR(9, c);
         }
-        // tile end: pred, rel-L2 loss, backward query record of this thread's query
+        if constexpr (kItems) {     // fold group 1's partial predictions into group 0
+            if (wh == 1)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) s_pp[(hh * 128 + q4 * 32 + lane) * 3 + ch] = pp[hh][ch];
+            asm volatile("bar.sync 1, %0;" ::"r"(kEpiW * 32) : "memory");
+            if (wh == 0)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) pp[hh][ch] += s_pp[(hh * 128 + q4 * 32 + lane) * 3 + ch];
+        }
+        // tile end: pred, rel-L2 loss, backward query record of the thread's query (items: group 0
+        // finishes the queries of both halves)
         double loss_acc = 0.0;
-        const int qi = h * 128 + q4 * 32 + lane;
-        if (qi < tile) {
-            const int64_t bq = t * tile + qi;
-            pred[bq * 3] = pp[0];
-            pred[bq * 3 + 1] = pp[1];
-            pred[bq * 3 + 2] = pp[2];
-            if (targets) {
-                float* qr = qrec + bq * QS;
-                double ell = 0.0;
 #pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                    const double pv = pp[ch], dv = pv - (double)targets[bq * 3 + ch], den = pv * pv + (double)eps;
-                    ell += dv * dv / den;
-                    qr[N + ch] = (float)(2.0 * dv / den * inv3n);
+        for (int hh = 0; hh < NIT; ++hh) {
+            const int qi = kItems ? hh * 128 + q4 * 32 + lane : wh * 128 + q4 * 32 + lane;
+            if ((!kItems || wh == 0) && qi < tile) {
+                const int64_t bq = t * tile + qi;
+                pred[bq * 3] = pp[hh][0];
+                pred[bq * 3 + 1] = pp[hh][1];
+                pred[bq * 3 + 2] = pp[hh][2];
+                if (targets) {
+                    float* qr = qrec + bq * QS;
+                    double ell = 0.0;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const double pv = pp[hh][ch], dv = pv - (double)targets[bq * 3 + ch], den = pv * pv + (double)eps;
+                        ell += dv * dv / den;
+                        qr[N + ch] = (float)(2.0 * dv / den * inv3n);
+                    }
+                    ell *= inv3n;
+#pragma unroll
+                    for (int d = 0; d < N; ++d) qr[d] = queries[bq * N + d];
+                    qr[N + 3] = (float)ell;
+#pragma unroll
+                    for (int d = N + 4; d < QS; ++d) qr[d] = 0.f;
+                    loss_acc += ell;
                 }
-                ell *= inv3n;
-#pragma unroll
-                for (int d = 0; d < N; ++d) qr[d] = queries[bq * N + d];
-                qr[N + 3] = (float)ell;
-#pragma unroll
-                for (int d = N + 4; d < QS; ++d) qr[d] = 0.f;
-                loss_acc = ell;
             }
         }
         if (targets) {

@@ -187,6 +187,20 @@ def test_brute_force_active_mask_vs_oracle(cuda, N, regime):
     assert not np.any(m & ~kept)
 
 
+@pytest.mark.parametrize("N", list(range(1, 17)))
+def test_tc_forward_every_dimension(cuda, N):
+    """The tcgen05 K5 launches and matches the oracle at every supported N (its shared-memory /
+    TMEM configuration is derived per N: chunk size, staging depth, B-ring stages)."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(N, 300, 512, sigma0=0.3)
+    hp = ndg.HotPath(N, projection_seed=2, forward="tc")
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    assert hp.last_forward_impl == "tc"
+    ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
+    assert _rel(res.pred.cpu().numpy(), ref["pred"]) < RTOL
+    assert abs(res.loss - ref["loss"]) <= RTOL * abs(ref["loss"])
+
+
 @pytest.mark.parametrize("fwd", ["fp32", "tc"])
 def test_cfg1_full_size_vs_c_oracle(cuda, fwd):
     """BASELINE.json configs[0] at full size: 6-D, 4096 Gaussians, 16384 queries (64 tiles)."""
