@@ -114,8 +114,14 @@ int ndg_cull_compact(int64_t T, int64_t Gev, const uint32_t* mask, const int64_t
  * size the mean divides by (3 * n_total entries).
  */
 int ndg_forward(int n, int64_t B, int tile, const float* queries, const float* targets, const float* rec,
-                const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total, float* pred, float* qrec,
-                double* loss_partial, void* stream);
+                int centred, const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total, float* pred,
+                float* qrec, double* loss_partial, void* stream);
+
+/* K1c: records for the centred FP32 kernels (`centred` = 1 in ndg_forward / ndg_backward): a copy of
+ * rec whose nb2 pair of row i holds (m_hi, m_lo), the float32 head and tail of mean64, so the first
+ * forward-substitution term is rho ((x - m_hi) - m_lo) instead of the cancelling rho x + nb2 (very
+ * sharp Gaussians; the engine decides from ndg_tc_records' conditioning). */
+int ndg_centre_records(int n, int64_t Gev, const double* mean64, const float* rec, float* rec_c, void* stream);
 
 /* Tensor-core records (float32 [Gev][N*pad8(N+1) + 4], rows stored plane-major [K/4][N][4]):
  * Ahat_e = [C L^-1 | C L^-1 (1/2 - m)] from K1's
@@ -141,7 +147,7 @@ int ndg_loss_finalize(int64_t T, const double* loss_partial, double* loss, void*
  * statistics S, t, gA and the density-control statistics, then adds them to accum[Gev][A]
  * (float64, zeroed by the caller).
  */
-int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec, const int64_t* offsets,
+int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec, int centred, const int64_t* offsets,
                  const int32_t* idx, const int64_t* chunk_offsets, int64_t n_chunks, double* accum, void* stream);
 
 /*

@@ -28,7 +28,7 @@ __host__ __device__ constexpr int srow_start(int i) {   // sum_{r<i} (r/2 + 1): 
 #define NDG_BWD_MINB 3   // CTAs per SM the register budget is sized for (N <= 10); tuning builds only
 #endif
 
-template <int N>
+template <int N, bool CTR>
 __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     backward_kernel(int64_t T, int tile, const float* __restrict__ qrec, const float* __restrict__ rec,
                     const int64_t* __restrict__ offsets, const int32_t* __restrict__ idx,
@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
         float s2 = 0.f;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            float acc = fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]);
+            // centred records hold (m_hi, m_lo) in the nb2 slots: z = rho ((x - m_hi) - m_lo), no cancellation
+            float acc = CTR ? r[rec_rho(N) + i] * ((xq[i] - r[rec_nb2(N) + 2 * i]) - r[rec_nb2(N) + 2 * i + 1])
+                            : fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]);
 #pragma unroll
             for (int k = 0; k < i; ++k) acc = fmaf(r[rec_l(N, i, k)], (k & 1) ? z2[k / 2].y : z2[k / 2].x, acc);
             if (i & 1) z2[i / 2].y = acc;
@@ -157,34 +159,35 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
 }
 
 template <int N>
-int launch_backward(int64_t B, int tile, const float* qrec, const float* rec, const int64_t* off, const int32_t* idx,
-                    const int64_t* chunk_off, int64_t n_chunks, double* accum, cudaStream_t st) {
+int launch_backward(int64_t B, int tile, const float* qrec, const float* rec, int centred, const int64_t* off,
+                    const int32_t* idx, const int64_t* chunk_off, int64_t n_chunks, double* accum, cudaStream_t st) {
     const int64_t T = B / tile;
     const size_t smem = sizeof(float) * tile * qrec_floats(N);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(backward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(backward_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(backward_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     NDG_REQUIRE(n_chunks <= 0x7fffffffLL, "too many backward work items");
-    backward_kernel<N><<<(unsigned)n_chunks, kBwdThreads, smem, st>>>(T, tile, qrec, rec, off, idx, chunk_off,
-                                                                       accum);
+    auto kern = centred ? backward_kernel<N, true> : backward_kernel<N, false>;
+    kern<<<(unsigned)n_chunks, kBwdThreads, smem, st>>>(T, tile, qrec, rec, off, idx, chunk_off, accum);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }
 
 }  // namespace
 
-extern "C" int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec, const int64_t* offsets,
-                            const int32_t* idx, const int64_t* chunk_offsets, int64_t n_chunks, double* accum,
-                            void* stream) {
+extern "C" int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec, int centred,
+                            const int64_t* offsets, const int32_t* idx, const int64_t* chunk_offsets, int64_t n_chunks,
+                            double* accum, void* stream) {
     NDG_REQUIRE(tile >= 1 && tile <= 1024 && B % tile == 0, "tile must be in 1..1024 and divide B");
     if (B == 0 || n_chunks == 0) return NDG_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     switch (n) {
 #define NDG_CASE(NN) \
     case NN:         \
-        return launch_backward<NN>(B, tile, qrec, rec, offsets, idx, chunk_offsets, n_chunks, accum, st);
+        return launch_backward<NN>(B, tile, qrec, rec, centred, offsets, idx, chunk_offsets, n_chunks, accum, st);
         NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
         NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
 #undef NDG_CASE

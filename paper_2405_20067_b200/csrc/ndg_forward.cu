@@ -40,7 +40,7 @@ template <> struct FwdCfg<16> { static constexpr int QPT = 2, NT = 128, STAGES =
 // landed the stage's records (expect_tx by lane 0 of warp 0); empty[s] completes when every warp
 // has finished reading the stage (one arrive per warp). Only warp 0 (the producer) ever waits on
 // empty[s], just before refilling it; consumer warps never wait on each other.
-template <int N, int QPT, int NT, int STAGES>
+template <int N, int QPT, int NT, int STAGES, bool CTR>
 __global__ void __launch_bounds__(NT)
     forward_kernel(int tile, const float* __restrict__ queries, const float* __restrict__ targets,
                    const float* __restrict__ rec, const int64_t* __restrict__ offsets,
@@ -131,8 +131,15 @@ __global__ void __launch_bounds__(NT)
                     float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int i = 0; i < N; ++i) {
-                        float2 acc = __ffma2_rn(make_float2(r[rec_rho(N) + i], r[rec_rho(N) + i]), x2[jp][i],
-                                                make_float2(r[rec_nb2(N) + 2 * i], r[rec_nb2(N) + 2 * i + 1]));
+                        float2 acc;
+                        if constexpr (CTR) {   // centred records: slots (m_hi, m_lo), z = rho ((x - m_hi) - m_lo)
+                            const float2 d = __fadd2_rn(__fadd2_rn(x2[jp][i], make_float2(-r[rec_nb2(N) + 2 * i], -r[rec_nb2(N) + 2 * i])),
+                                                        make_float2(-r[rec_nb2(N) + 2 * i + 1], -r[rec_nb2(N) + 2 * i + 1]));
+                            acc = __fmul2_rn(make_float2(r[rec_rho(N) + i], r[rec_rho(N) + i]), d);
+                        } else {
+                            acc = __ffma2_rn(make_float2(r[rec_rho(N) + i], r[rec_rho(N) + i]), x2[jp][i],
+                                             make_float2(r[rec_nb2(N) + 2 * i], r[rec_nb2(N) + 2 * i + 1]));
+                        }
 #pragma unroll
                         for (int k = 0; k < i; ++k)
                             acc = __ffma2_rn(make_float2(r[rec_l(N, i, k)], r[rec_l(N, i, k)]), z[k], acc);
@@ -202,16 +209,17 @@ __global__ void __launch_bounds__(NT)
 }
 
 template <int N>
-int launch_forward(int64_t B, int tile, const float* q, const float* tgt, const float* rec, const int64_t* off,
-                   const int32_t* idx, float eps, int64_t n_total, float* pred, float* qrec, double* lp,
-                   cudaStream_t st) {
+int launch_forward(int64_t B, int tile, const float* q, const float* tgt, const float* rec, int centred,
+                   const int64_t* off, const int32_t* idx, float eps, int64_t n_total, float* pred, float* qrec,
+                   double* lp, cudaStream_t st) {
     using C = FwdCfg<N>;
     const int64_t T = B / tile;
     const size_t smem = sizeof(float) * C::STAGES * kChunk * rec_floats(N);
-    auto kern = forward_kernel<N, C::QPT, C::NT, C::STAGES>;
+    auto kern = centred ? forward_kernel<N, C::QPT, C::NT, C::STAGES, true> : forward_kernel<N, C::QPT, C::NT, C::STAGES, false>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(forward_kernel<N, C::QPT, C::NT, C::STAGES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(forward_kernel<N, C::QPT, C::NT, C::STAGES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     kern<<<(unsigned)T, C::NT, smem, st>>>(tile, q, tgt, rec, off, idx, eps, 1.0 / (3.0 * (double)n_total), pred,
@@ -223,8 +231,8 @@ int launch_forward(int64_t B, int tile, const float* q, const float* tgt, const 
 }  // namespace
 
 extern "C" int ndg_forward(int n, int64_t B, int tile, const float* queries, const float* targets, const float* rec,
-                           const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total, float* pred,
-                           float* qrec, double* loss_partial, void* stream) {
+                           int centred, const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total,
+                           float* pred, float* qrec, double* loss_partial, void* stream) {
     NDG_REQUIRE(tile >= 1 && tile <= 1024 && B % tile == 0, "tile must be in 1..1024 and divide B");
     NDG_REQUIRE(!targets || (qrec && loss_partial && n_total > 0), "targets need qrec, loss_partial, n_total");
     if (B == 0) return NDG_OK;
@@ -232,7 +240,8 @@ extern "C" int ndg_forward(int n, int64_t B, int tile, const float* queries, con
     switch (n) {
 #define NDG_CASE(NN) \
     case NN:         \
-        return launch_forward<NN>(B, tile, queries, targets, rec, offsets, idx, eps, n_total, pred, qrec, loss_partial, st);
+        return launch_forward<NN>(B, tile, queries, targets, rec, centred, offsets, idx, eps, n_total, pred, qrec, \
+                                  loss_partial, st);
         NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
         NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
 #undef NDG_CASE

@@ -5,15 +5,18 @@
 // Ahat_e = [C L_e^-1 | C L_e^-1 (1/2 - m_e)] (K1 + ndg_tc_records, float64 -> float32) and the
 // query features xhat_q = [x_q - 1/2, 1],
 //     z~[q, (e,i)] = sum_k xhat_q[k] Ahat_e[i][k]      (= C * z_i of L z = x - m)
-// computed by tcgen05.mma (M = 128 queries, N = 128 columns = floor(128/N) Gaussians x N rows,
-// K = pad8(N+1)) in 3xTF32 (hi*hi + hi*lo + lo*hi, fp32 accumulate in TMEM): tools/
-// tc_precision_study.py shows <= 4.4e-5 block-relative error on pred at sigma 0.02 (bar 1e-4).
-// The epilogue warps read z~ rows from TMEM and finish on the FP32 pipe:
+// computed by tcgen05.mma (M = 128 queries of one tile half, N = 224 columns = C Gaussians x N rows in
+// two 16-aligned groups, K = pad8(N+1)) in 3xTF32 (hi*hi + hi*lo + lo*hi, fp32 accumulate in TMEM):
+// tools/tc_precision_study.py shows <= 4.4e-5 block-relative error on pred at sigma 0.02 (bar 1e-4);
+// HotPath's conditioning guard keeps sharper mixtures on the FP32 pipe. The epilogue warps read z~
+// rows from TMEM and finish on the FP32 pipe:
 //     s~ = sum_i z~_i^2 (FFMA2 over column pairs),  g = ex2(-s~),  pred += g * a.
 //
-// Pipeline (384 threads): TMA bulk copies of whole candidate records into a staging ring, splitter
-// warps convert them to the hi/lo K-major B planes, one lane issues the MMAs, eight epilogue warps
-// drain TMEM (accumulators double-buffered: 2 x 2 halves x 128 columns = 512).
+// Pipeline (416 threads, one CTA per tile of 256 queries): two producer warps gather whole candidate
+// records into a staging ring (cp.async.bulk), two splitter warps convert them to the hi/lo K-major B
+// planes, one lane issues the MMAs of item (chunk, half) into TMEM buffer `half`, eight epilogue
+// warps (4 lane quarters x 2 Gaussian groups) drain TMEM (2 x 224 accumulator + 64 A columns = 512).
+// The hand-off timeline (tools/tc_trace.py) shows the tensor pipe ~85% busy per chunk.
 #include "ndg_tc.cuh"
 
 using namespace ndg;
@@ -28,7 +31,7 @@ namespace {
 #endif
 constexpr int kSplit = NDG_TC_SPLITTERS;   // splitter warps (2 .. 2 + kSplit - 1)
 constexpr int kEpi0 = 2 + kSplit;           // first epilogue warp (a multiple of 4: lane quarter = warp % 4)
-constexpr int kEpiW = 8;                    // epilogue warps (2 query halves x 4 lane quarters)
+constexpr int kEpiW = 8;                    // epilogue warps (2 Gaussian groups x 4 lane quarters)
 static_assert(kEpi0 % 4 == 0, "epilogue warp w must own TMEM lane quarter w % 4");
 #ifndef NDG_TC_PRODUCERS
 #define NDG_TC_PRODUCERS 2
@@ -40,10 +43,7 @@ constexpr int kProd = NDG_TC_PRODUCERS;
 constexpr int kTcWarps = kEpi0 + kEpiW + (kProd - 1);
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcStaging = NDG_TC_STAGING;   // raw-record staging ring depth (capped per N by the smem budget)
-#ifndef NDG_TC_TBUF
-#define NDG_TC_TBUF 2
-#endif
-constexpr int kTBuf = NDG_TC_TBUF;            // TMEM accumulator buffers (x 2 query halves)
+constexpr int kTBuf = 2;                      // TMEM accumulator buffers: one per query half
 
 constexpr int kARing = 8;                     // colour ring depth (independent of the B ring)
 
@@ -62,35 +62,29 @@ constexpr unsigned kTraceCta = 300;
     } while (0)
 #endif
 
-#ifndef NDG_TC_ITEMS
-#define NDG_TC_ITEMS 1
-#endif
-// Items mode: a chunk's MMA covers twice the Gaussians (N = 224 at N = 10) and one query half at a time
-// (item = (chunk, half) -> TMEM buffer = half), so each tcgen05.mma does twice the work per issue; the
-// epilogue splits a chunk's Gaussians into two groups per lane quarter (columns [0, CG*N) and
-// [GOFF, GOFF + (C-CG)*N), GOFF 16-aligned).
-constexpr bool kItems = NDG_TC_ITEMS;
+// Items: a chunk's z-GEMM covers C Gaussians (MMA N = 224 at N = 10) and runs one query half at a time
+// (item = (chunk, half) -> TMEM buffer = half), so each tcgen05.mma does as much work per issue as TMEM
+// allows; the epilogue splits a chunk's Gaussians into two groups per lane quarter (columns
+// [0, CG*N) and [GOFF, GOFF + (C-CG)*N), GOFF 16-aligned).
 
 template <int N>
 struct TcCfg {
     static constexpr int K = tc_k(N);
     static constexpr int P = K / 4;
     static constexpr int KS = K / 8;
-    // TMEM: A operand (2 halves x hi/lo x K columns) + kTBuf buffers x 2 halves x NCOL accumulator columns
-    // (items: kTBuf buffers x NCOL, one per query half)
+    // TMEM: A operand (2 halves x hi/lo x K columns) + one NCOL-column accumulator buffer per query half
     static constexpr int ACOLS = 4 * K;
-    static constexpr int NCOL = kItems ? ((512 - ACOLS) / kTBuf) & ~15 : ((512 - ACOLS) / (2 * kTBuf)) & ~15;
-    static constexpr int A0 = kItems ? kTBuf * NCOL : 2 * kTBuf * NCOL;   // first A column
-    static constexpr int ROWS = kItems ? NCOL : 128;                      // B operand rows per plane
-    static constexpr int PLANE = ROWS * 16;
+    static constexpr int NCOL = ((512 - ACOLS) / kTBuf) & ~15;           // MMA N (224 at N = 10)
+    static constexpr int A0 = kTBuf * NCOL;                              // first A column
+    static constexpr int PLANE = NCOL * 16;                              // B plane: NCOL rows x 16 B
     static constexpr int items_c() {
         int c = NCOL / N < 32 ? NCOL / N : 32;
         while (c > 1 && ((((c + 1) / 2) * N + 15) / 16) * 16 + (c - (c + 1) / 2) * N > NCOL) --c;
         return c;
     }
-    static constexpr int C = kItems ? items_c() : (NCOL / N < 32 ? NCOL / N : 32);
-    static constexpr int CG = kItems ? (C + 1) / 2 : C;                   // Gaussians of epilogue group 0
-    static constexpr int GOFF = kItems ? ((CG * N + 15) / 16) * 16 : 0;   // first column of group 1
+    static constexpr int C = items_c();                                  // Gaussians per chunk (<= 32 producer lanes)
+    static constexpr int CG = (C + 1) / 2;                               // Gaussians of epilogue group 0
+    static constexpr int GOFF = ((CG * N + 15) / 16) * 16;               // first column of group 1
     static constexpr int RT = tc_rec_floats(N);       // floats per raw record (rows | a | pad)
     static constexpr size_t kRing = (size_t)kARing * C * 16;
     static constexpr size_t kSlot = (size_t)C * RT * 4;
@@ -102,7 +96,7 @@ struct TcCfg {
     static constexpr int STG = (kFixed + kTcStaging * kSlot <= kBudget) ? kTcStaging : (int)((kBudget - kFixed) / kSlot);
     static_assert(STG >= 2, "shared-memory budget too small for the staging ring");
     static_assert(kARing >= STAGES + kTBuf + 1, "colour-slot reuse relies on the B-stage wait (splitters)");
-    static_assert(!kItems || kTBuf == 2, "items mode keeps one TMEM buffer per query half");
+    static_assert(kTBuf == 2, "one TMEM accumulator buffer per query half");
 };
 
 template <int N>
@@ -111,9 +105,10 @@ constexpr size_t tc_smem_bytes() {
     return C_::kFixed + (size_t)C_::STG * C_::kSlot;
 }
 
-// Warp roles: 0 = TMA producer (one cp.async.bulk per candidate record into the staging ring),
-// 1 = TMEM allocator + MMA issuer, 2..kEpi0-1 = splitters (staging -> hi/lo K-major B planes + colours),
-// kEpi0.. = epilogue (warp w: query half (w-kEpi0)/4, TMEM lane quarter w%4).
+// Warp roles: 0 and kTcWarps-1 = TMA producers (even / odd chunks; one cp.async.bulk per candidate
+// record into the staging ring), 1 = TMEM allocator + MMA issuer, 2..kEpi0-1 = splitters (staging ->
+// hi/lo K-major B planes + colours), kEpi0..kEpi0+7 = epilogue (warp w: Gaussian group (w-kEpi0)/4,
+// TMEM lane quarter w%4; the A-operand prologue writes query half (w-kEpi0)/4).
 template <int N>
 __global__ void __launch_bounds__(kTcThreads, 1)
     forward_tc_kernel(int tile, const float* __restrict__ queries, const float* __restrict__ targets,
@@ -136,7 +131,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __shared__ __align__(8) uint64_t tfull_bar[kTBuf], tempty_bar[kTBuf];
     __shared__ uint32_t s_tbase;
     __shared__ double s_loss[8];
-    __shared__ float s_pp[kItems ? 256 * 3 : 1];
+    __shared__ float s_pp[256 * 3];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t t = blockIdx.x;
@@ -225,24 +220,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (lane == 0) {
             const uint32_t b_base = smem_u32(sB);
             for (int c = 0; c < nchunks; ++c) {
-                const int s = c % kTcStages, b = c % kTBuf;
+                const int s = c % kTcStages;
                 mbar_wait(&full_bar[s], (uint32_t)(c / kTcStages) & 1);
                 NDG_TR(3, c);
-                if constexpr (!kItems) {
-                    if (c >= kTBuf) mbar_wait(&tempty_bar[b], (uint32_t)((c / kTBuf) - 1) & 1);
-                }
                 NDG_TR(4, c);
-                tc::fence_after();
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    uint32_t d;
-                    if constexpr (kItems) {          // item (c, h) -> TMEM buffer h
-                        if (c >= 1) mbar_wait(&tempty_bar[h], (uint32_t)(c - 1) & 1);
-                        tc::fence_after();
-                        d = tbase + (uint32_t)(h * kNCol);
-                    } else {
-                        d = tbase + (uint32_t)((b * 2 + h) * kNCol);
-                    }
+                for (int h = 0; h < 2; ++h) {              // item (c, h) -> TMEM buffer h
+                    if (c >= 1) mbar_wait(&tempty_bar[h], (uint32_t)(c - 1) & 1);
+                    tc::fence_after();
+                    const uint32_t d = tbase + (uint32_t)(h * kNCol);
                     const uint32_t ahi = tbase + (uint32_t)(kA0 + h * 2 * K), alo = ahi + K;
 #pragma unroll
                     for (int ks = 0; ks < KS; ++ks) {
@@ -254,10 +240,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         tc::mma_tf32_ta(d, alo + 8 * ks, bhi, IDESC, 1u);
 #endif
                     }
-                    if constexpr (kItems) tc::commit(&tfull_bar[h]);   // item (c, h) is ready
+                    tc::commit(&tfull_bar[h]);             // item (c, h) is ready
                 }
-                tc::commit(&empty_bar[s]);      // B stage s may be refilled
-                if constexpr (!kItems) tc::commit(&tfull_bar[b]);      // accumulators of buffer b are ready
+                tc::commit(&empty_bar[s]);                 // B stage s may be refilled
                 NDG_TR(5, c);
             }
         }
@@ -276,7 +261,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int g = u / (N * P), rem = u - g * (N * P);
             const int p = rem / N, i = rem - p * N;
             src_off[k] = g * RT + rem * 4;
-            const int row = (kItems && g >= CG) ? GOFF + (g - CG) * N + i : g * N + i;   // D column of (g, i)
+            const int row = g >= CG ? GOFF + (g - CG) * N + i : g * N + i;   // D column of (g, i)
             dst_off[k] = p * kPlane + row * 16;
         }
         for (int c = 0; c < nchunks; ++c) {
@@ -335,27 +320,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else {
         // ------------------------------ epilogue -----------------------------------------------
-        // warp (wh, q4): TMEM lane quarter q4. Default: wh = query half, all C Gaussians of a chunk.
-        // Items: wh = Gaussian group, for both halves' items; pp[hh] is the partial prediction of the
-        // thread's query in half hh (group 1 hands its partials to group 0 at tile end).
+        // warp (wh, q4): TMEM lane quarter q4, Gaussian group wh of both halves' items; pp[hh] is the
+        // partial prediction of the thread's query in half hh (group 1 hands its partials to group 0
+        // at tile end).
         const int wh = (warp - kEpi0) >> 2, q4 = warp & 3;
-        constexpr int NGW = kItems ? CG : C;            // Gaussian slots per warp per item
+        constexpr int NGW = CG;                         // Gaussian slots per warp per item
         constexpr int NLD = (NGW * N + 15) / 16;
-        constexpr int NIT = kItems ? 2 : 1;             // items per chunk
+        constexpr int NIT = 2;                          // items per chunk
         float pp[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-        const int g0 = kItems ? wh * CG : 0;
-        const int ngw = kItems ? (wh ? C - CG : CG) : C;
+        const int g0 = wh * CG;
+        const int ngw = wh ? C - CG : CG;
         for (int c = 0; c < nchunks; ++c) {
             const int as = c % kARing;
             const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
 #pragma unroll
             for (int it = 0; it < NIT; ++it) {
-                const int b = kItems ? it : c % kTBuf;
-                mbar_wait(&tfull_bar[b], kItems ? (uint32_t)c & 1 : (uint32_t)(c / kTBuf) & 1);
+                const int b = it;
+                mbar_wait(&tfull_bar[b], (uint32_t)c & 1);
                 if (warp == kEpi0 && lane == 0 && it == 0) NDG_TR(6, c);
                 tc::fence_after();
                 float v[NLD * 16];
-                const uint32_t col = kItems ? (uint32_t)(it * kNCol + wh * GOFF) : (uint32_t)((b * 2 + wh) * kNCol);
+                const uint32_t col = (uint32_t)(it * kNCol + wh * GOFF);
                 const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + col;
 #ifdef NDG_TCX_NOLD
                 for (int j = 0; j < NLD * 16; ++j) v[j] = (float)(ta + j);
@@ -390,7 +375,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     pp[it][1] = fmaf(gv, av.y, pp[it][1]);
                     pp[it][2] = fmaf(gv, av.z, pp[it][2]);
                 };
-                if (n_in == C && (!kItems || C == 2 * CG)) {      // full chunk: no per-Gaussian predicates
+                if (n_in == C && C == 2 * CG) {       // full chunk: no per-Gaussian predicates
 #pragma unroll
                     for (int gl = 0; gl < NGW; ++gl) gauss(gl);
                 } else {
@@ -405,7 +390,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (warp == kEpi0 && lane == 0) NDG_TR(8, c);
             if (warp == kEpi0 + 7 && lane == 0) NDG_TR(9, c);
         }
-        if constexpr (kItems) {     // fold group 1's partial predictions into group 0
+        {                            // fold group 1's partial predictions into group 0
             if (wh == 1)
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh)
@@ -418,13 +403,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) pp[hh][ch] += s_pp[(hh * 128 + q4 * 32 + lane) * 3 + ch];
         }
-        // tile end: pred, rel-L2 loss, backward query record of the thread's query (items: group 0
-        // finishes the queries of both halves)
+        // tile end: pred, rel-L2 loss, backward query records (group 0 finishes both halves' queries)
         double loss_acc = 0.0;
 #pragma unroll
         for (int hh = 0; hh < NIT; ++hh) {
-            const int qi = kItems ? hh * 128 + q4 * 32 + lane : wh * 128 + q4 * 32 + lane;
-            if ((!kItems || wh == 0) && qi < tile) {
+            const int qi = hh * 128 + q4 * 32 + lane;
+            if (wh == 0 && qi < tile) {
                 const int64_t bq = t * tile + qi;
                 pred[bq * 3] = pp[hh][0];
                 pred[bq * 3 + 1] = pp[hh][1];

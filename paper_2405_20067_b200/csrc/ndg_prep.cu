@@ -250,6 +250,35 @@ extern "C" int ndg_tile_bounds(int n, int64_t B, int tile, const float* queries,
 }
 
 // ---------------------------------------------------------------------------------------------
+// K1c centred records for very sharp mixtures (HotPath centres the FP32 kernels when the z-GEMM
+// conditioning says rho x + nb2 would cancel): a copy of K1's records with the nb2 pair of row i
+// replaced by (m_hi, m_lo), the float32 head and tail of the float64 mean, so the FP32 K5 / K7 evaluate
+// z_i = rho_i ((x_i - m_hi) - m_lo) + sum_k l_ik z_k, exact near the Gaussian (Sterbenz).
+// ---------------------------------------------------------------------------------------------
+__global__ void centre_records_kernel(int n, int64_t Gev, const double* __restrict__ mean64,
+                                      const float* __restrict__ rec, float* __restrict__ rec_c) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= Gev) return;
+    const int RS = rec_floats(n);
+    for (int k = 0; k < RS; ++k) rec_c[e * RS + k] = rec[e * RS + k];
+    for (int i = 0; i < n; ++i) {
+        const double m = mean64[e * n + i];
+        const float hi = (float)m;
+        rec_c[e * RS + rec_nb2(n) + 2 * i] = hi;
+        rec_c[e * RS + rec_nb2(n) + 2 * i + 1] = (float)(m - (double)hi);
+    }
+}
+
+extern "C" int ndg_centre_records(int n, int64_t Gev, const double* mean64, const float* rec, float* rec_c,
+                                  void* stream) {
+    if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
+    if (Gev == 0) return NDG_OK;
+    centre_records_kernel<<<(unsigned)((Gev + 127) / 128), 128, 0, as_stream(stream)>>>(n, Gev, mean64, rec, rec_c);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
 // K4a cull mask: cull_tile for all tiles. Thread = evaluated Gaussian, CTA =
 // 256 Gaussians x TILES tiles; the tiles' intervals sit in shared memory and are broadcast, the
 // Gaussian's (m_r, thr) live in registers for k <= 16 (shared memory otherwise). Culled iff any

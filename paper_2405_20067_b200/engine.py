@@ -87,6 +87,7 @@ class EvalRecords:
     rec_tc: torch.Tensor = None   # [Gev, N*pad8(N+1) + 4] float32 Ahat records + colour (tensor-core forward)
     tc_cond: torch.Tensor = None   # [3] float64: [max, sum of squares, count] of B_e (ndg_tc_records)
     tc_cond_host: tuple = None     # read back with the step's one mid-pipeline sync
+    rec_c: torch.Tensor = None     # K1c centred records, built on demand (very sharp mixtures)
 
     def tc_conditioning(self) -> float:
         """RMS over live Gaussians of B_e, the z-GEMM's conditioning (inf without tensor-core records)."""
@@ -212,6 +213,7 @@ class HotPath:
         self.backward_impl = "tc" if bwd == "tc" and K.load().ndg_backward_tc_supported(self.n) else "fp32"
         self._recs = None    # the last activation: its conditioning bound rides on the cull's read-back
         self.last_forward_impl = self.last_backward_impl = None   # what the last step ran
+        self.last_centred = False
         self.events = None   # when a dict: {"forward": [(start, end), ...], "backward": [...]} CUDA events
 
     def enable_kernel_timing(self, on: bool = True):
@@ -243,15 +245,13 @@ class HotPath:
         K.call("ndg_prologue", n, G, Gev, mix.amp_mode, _p(mix.params), _p(mix.child), _p(mix.flags), _p(rec),
                _p(mean64), _p(chol64), _p(eflags), _p(self.status), _stream())
         rec_tc = None
-        if self.forward_impl == "tc" or self.backward_impl == "tc":
-            kk = ((n + 1 + 7) // 8) * 8
-            rec_tc = torch.empty(Gev, n * kk + 4, dtype=torch.float32, device=dev)
-            cond = torch.zeros(3, dtype=torch.float64, device=dev)
-            K.call("ndg_tc_records", n, Gev, _p(mean64), _p(chol64), _p(eflags), _p(rec), _p(rec_tc), _p(cond),
-                   _stream())
-            recs = EvalRecords(Gev, rec, mean64, chol64, eflags, rec_tc, cond)
-        else:
-            recs = EvalRecords(Gev, rec, mean64, chol64, eflags)
+        # tensor-core records + the conditioning statistic: the TC kernels and the FP32 kernels'
+        # centring decision both read it
+        kk = ((n + 1 + 7) // 8) * 8
+        rec_tc = torch.empty(Gev, n * kk + 4, dtype=torch.float32, device=dev)
+        cond = torch.zeros(3, dtype=torch.float64, device=dev)
+        K.call("ndg_tc_records", n, Gev, _p(mean64), _p(chol64), _p(eflags), _p(rec), _p(rec_tc), _p(cond), _stream())
+        recs = EvalRecords(Gev, rec, mean64, chol64, eflags, rec_tc, cond)
         self._recs = recs
         return recs
 
@@ -261,6 +261,20 @@ class HotPath:
     # at 842 (2.3e-4, out of tolerance). The moments K7 loses ~B^2 and is held to broad mixtures.
     TC_FORWARD_MAX_BOUND = 200.0      # RMS of B_e; error ~2e-7 * RMS (measured 4.4e-5 @ 256, 2.3e-4 @ 842)
     TC_BACKWARD_MAX_BOUND = 20.0      # moments K7: error ~8e-8 * RMS^2 (9.7e-5 vs the FP32 K7 @ 35)
+
+    # The FP32 kernels' first term rho x + nb2 cancels like the z-GEMM (error ~1.4e-7 * RMS(B), e.g.
+    # 1.45e-4 at RMS 1022 for the sigma 7e-4 mixture of tests/test_gpu_fuzz.py); past this bound they
+    # run on centred records, z = rho ((x - m_hi) - m_lo), which loses nothing near the Gaussian.
+    FP32_CENTRE_BOUND = 150.0
+
+    def centred_records(self, recs: EvalRecords):
+        """K1c records (or None) for the FP32 K5 / K7 of this step."""
+        if recs.tc_conditioning() <= self.FP32_CENTRE_BOUND:
+            return None
+        if recs.rec_c is None:
+            recs.rec_c = torch.empty_like(recs.rec)
+            K.call("ndg_centre_records", self.n, recs.Gev, _p(recs.mean64), _p(recs.rec), _p(recs.rec_c), _stream())
+        return recs.rec_c
 
     def forward_tc_ok(self, recs: EvalRecords) -> bool:
         """Whether this step's K5 runs on the tensor cores (else the FP32-pipe K5, same contract)."""
@@ -367,7 +381,10 @@ class HotPath:
             K.call("ndg_forward_tc", self.n, B, self.tile, _p(queries), _p(targets), _p(recs.rec_tc),
                    _p(cl.offsets), _p(cl.idx), self.eps, int(n_total or B), _p(pred), _p(qrec), _p(loss_part), _stream())
         else:
-            K.call("ndg_forward", self.n, B, self.tile, _p(queries), _p(targets), _p(recs.rec), _p(cl.offsets),
+            rc = self.centred_records(recs)
+            self.last_centred = rc is not None
+            K.call("ndg_forward", self.n, B, self.tile, _p(queries), _p(targets), _p(recs.rec if rc is None else rc),
+                   int(rc is not None), _p(cl.offsets),
                    _p(cl.idx), self.eps, int(n_total or B), _p(pred), _p(qrec), _p(loss_part), _stream())
         self._ev("forward", 1)
         return pred, qrec, loss_part
@@ -390,7 +407,10 @@ class HotPath:
             K.call("ndg_moments_to_zspace", self.n, recs.Gev, _p(recs.mean64), _p(recs.chol64), _p(recs.eflags),
                    _p(accum), _stream())
         else:
-            K.call("ndg_backward", self.n, B, self.tile, _p(qrec), _p(recs.rec), _p(cl.offsets), _p(cl.idx),
+            rc = self.centred_records(recs)
+            self.last_centred = rc is not None
+            K.call("ndg_backward", self.n, B, self.tile, _p(qrec), _p(recs.rec if rc is None else rc),
+                   int(rc is not None), _p(cl.offsets), _p(cl.idx),
                    _p(cl.chunk_offsets), cl.n_chunks, _p(accum), _stream())
             self._ev("backward", 1)
         K.call("ndg_epilogue", self.n, mix.G, recs.Gev, mix.amp_mode, _p(mix.params), _p(mix.child), _p(mix.flags),

@@ -36,9 +36,10 @@ SIGNATURES = {
     "ndg_cull_mask": [_L, _I, _L, _P, _P, _P, _P, _P, _P, _P],
     "ndg_scan_counts": [_L, _P, _P, _P, _P],
     "ndg_cull_compact": [_L, _L, _P, _P, _P, _P],
-    "ndg_forward": [_I, _L, _I, _P, _P, _P, _P, _P, _F, _L, _P, _P, _P, _P],
+    "ndg_forward": [_I, _L, _I, _P, _P, _P, _I, _P, _P, _F, _L, _P, _P, _P, _P],
+    "ndg_centre_records": [_I, _L, _P, _P, _P, _P],
     "ndg_loss_finalize": [_L, _P, _P, _P],
-    "ndg_backward": [_I, _L, _I, _P, _P, _P, _P, _P, _L, _P, _P],
+    "ndg_backward": [_I, _L, _I, _P, _P, _I, _P, _P, _P, _L, _P, _P],
     "ndg_backward_tc_supported": [_I],
     "ndg_backward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _P],
     "ndg_moments_to_zspace": [_I, _L, _P, _P, _P, _P, _P],
@@ -89,7 +90,7 @@ class NdgLaunchError(RuntimeError):
 # entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
 LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_scan_counts",
              "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_backward", "ndg_backward_tc",
-             "ndg_moments_to_zspace", "ndg_active_mask", "ndg_epilogue", "ndg_adam",
+             "ndg_moments_to_zspace", "ndg_active_mask", "ndg_centre_records", "ndg_epilogue", "ndg_adam",
              "ndg_fp32_probe", "ndg_tf32_probe"}
 launch_count = 0
 

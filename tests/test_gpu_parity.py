@@ -187,6 +187,22 @@ def test_brute_force_active_mask_vs_oracle(cuda, N, regime):
     assert not np.any(m & ~kept)
 
 
+@pytest.mark.parametrize("N,G,fwd,sigma0", [(1, 400, "tc", None), (1, 400, "fp32", None), (2, 400, "tc", 0.002),
+                                              (4, 300, "fp32", 0.002), (10, 300, "tc", 0.004)])
+def test_very_sharp_mixture_centred_fp32(cuda, N, G, fwd, sigma0):
+    """sigma ~ 1e-3 of the domain: rho x + nb2 would cancel in float32, so the step runs the FP32 K5 /
+    K7 on centred records (HotPath.FP32_CENTRE_BOUND) and still meets the 1e-4 bar."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(N, G, 1024, children=True, regime="C", sigma0=sigma0)
+    hp = ndg.HotPath(N, projection_seed=2, forward=fwd)
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    assert hp.last_forward_impl == "fp32" and hp.last_centred
+    ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
+    assert _rel(res.pred.cpu().numpy(), ref["pred"]) < RTOL
+    _check_grads(N, res.grads.params.cpu().numpy(), ref["grad_parent"], "parent")
+    _check_grads(N, res.grads.child.cpu().numpy(), ref["grad_child"], "child")
+
+
 @pytest.mark.parametrize("N", list(range(1, 17)))
 def test_tc_forward_every_dimension(cuda, N):
     """The tcgen05 K5 launches and matches the oracle at every supported N (its shared-memory /
