@@ -163,11 +163,10 @@ int launch_backward(int64_t B, int tile, const float* qrec, const float* rec, in
                     const int32_t* idx, const int64_t* chunk_off, int64_t n_chunks, double* accum, cudaStream_t st) {
     const int64_t T = B / tile;
     const size_t smem = sizeof(float) * tile * qrec_floats(N);
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(backward_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(backward_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
     }
     NDG_REQUIRE(n_chunks <= 0x7fffffffLL, "too many backward work items");
     auto kern = centred ? backward_kernel<N, true> : backward_kernel<N, false>;

@@ -431,10 +431,9 @@ int launch_backward_tc(int64_t B, int tile, const float* qrec, const float* rec_
         const int64_t T = B / tile;
         const int halves = (tile + kQ - 1) / kQ;
         const size_t smem = bt_smem_bytes<N>();
-        static bool attr = false;
-        if (!attr) {
+        static DeviceOnce attr;
+        if (attr.first()) {
             cudaFuncSetAttribute(backward_tc_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
         }
         NDG_REQUIRE(T * halves <= 0x7fffffffLL, "too many tiles");
         backward_tc_kernel<N><<<(unsigned)(T * halves), kBtThreads, smem, st>>>(tile, halves, qrec, rec_tc, off, idx,

@@ -68,6 +68,21 @@ constexpr double kC = 0.84932180028801907;      // sqrt(0.5 * log2(e))
 
 }  // namespace ndg
 
+// Kernel attributes (e.g. the dynamic shared-memory opt-in) are per device: a launcher sets them the
+// first time it runs on each device of the process, thread-safely.
+#include <atomic>
+namespace ndg {
+struct DeviceOnce {
+    std::atomic<unsigned long long> mask{0};
+    bool first() {
+        int d = 0;
+        cudaGetDevice(&d);
+        const unsigned long long bit = 1ull << (d & 63);
+        return !(mask.fetch_or(bit) & bit);
+    }
+};
+}  // namespace ndg
+
 // error string (per-thread) defined in ndg_prep.cu
 extern "C" void ndg_set_last_error(const char* msg);
 

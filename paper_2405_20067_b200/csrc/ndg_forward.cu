@@ -216,11 +216,10 @@ int launch_forward(int64_t B, int tile, const float* q, const float* tgt, const 
     const int64_t T = B / tile;
     const size_t smem = sizeof(float) * C::STAGES * kChunk * rec_floats(N);
     auto kern = centred ? forward_kernel<N, C::QPT, C::NT, C::STAGES, true> : forward_kernel<N, C::QPT, C::NT, C::STAGES, false>;
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(forward_kernel<N, C::QPT, C::NT, C::STAGES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(forward_kernel<N, C::QPT, C::NT, C::STAGES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     kern<<<(unsigned)T, C::NT, smem, st>>>(tile, q, tgt, rec, off, idx, eps, 1.0 / (3.0 * (double)n_total), pred,
                                            qrec, lp);

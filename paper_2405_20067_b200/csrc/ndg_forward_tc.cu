@@ -457,10 +457,9 @@ int launch_forward_tc(int64_t B, int tile, const float* q, const float* tgt, con
                       cudaStream_t st) {
     const int64_t T = B / tile;
     const size_t smem = tc_smem_bytes<N>();
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(forward_tc_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     forward_tc_kernel<N><<<(unsigned)T, kTcThreads, smem, st>>>(tile, q, tgt, rec_tc, off, idx, eps,
                                                                 1.0 / (3.0 * (double)n_total), pred, qrec, lp);

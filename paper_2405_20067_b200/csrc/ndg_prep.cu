@@ -384,11 +384,10 @@ extern "C" int ndg_cull_mask(int64_t T, int k, int64_t Gev, const double* lo, co
     dim3 grid((unsigned)((Gev + kCullThreads - 1) / kCullThreads), (unsigned)((T + tiles - 1) / tiles));
     NDG_REQUIRE(grid.y <= 65535, "too many tiles for one cull launch");
     const size_t smem = sizeof(double) * (2 * tiles * k + (reg ? 0 : 2 * k * kCullThreads));
-    static thread_local bool attr_set = false;
-    if (!attr_set) {
+    static DeviceOnce attr_set;
+    if (attr_set.first()) {
         cudaFuncSetAttribute(cull_mask_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         cudaFuncSetAttribute(cull_mask_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        attr_set = true;
     }
     if (reg)
         cull_mask_kernel<true><<<grid, kCullThreads, smem, as_stream(stream)>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts);
