@@ -36,7 +36,7 @@ static_assert(kEpi0 % 4 == 0, "epilogue warp w must own TMEM lane quarter w % 4"
 #ifndef NDG_TC_PRODUCERS
 #define NDG_TC_PRODUCERS 2
 #endif
-// Producer warps: warp 0 and (with 2) the last warp. A cp.async.bulk gather issues through the uniform
+// Producer warps: warp 0 and the kProd - 1 warps after the epilogue. A cp.async.bulk gather issues through the uniform
 // datapath one record at a time, so one warp issuing all of a chunk's records paced the pipeline
 // (tools/tc_trace.py: half the gathers -> -10%); producer p takes chunks c = p (mod kProd).
 constexpr int kProd = NDG_TC_PRODUCERS;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc::fence_after();
     const uint32_t tbase = s_tbase;
 
-    if (warp == 0 || (kProd > 1 && warp == kTcWarps - 1)) {
+    if (warp == 0 || warp >= kEpi0 + kEpiW) {      // producers: warp 0 and the warps after the epilogue
         // ------------------------------ TMA producer -------------------------------------------
         // lane g < C owns candidate g of every chunk; its index is loaded two chunks ahead so the
         // dependent idx -> record address load never sits on the chunk's critical path.
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int64_t pos = beg + (int64_t)c * C + lane;
             return (lane < C && c < nchunks && pos < end) ? (int64_t)__ldg(idx + pos) : 0;
         };
-        const int pid = warp == 0 ? 0 : 1;
+        const int pid = warp == 0 ? 0 : warp - (kEpi0 + kEpiW) + 1;
         int64_t e0 = load_idx(pid), e1 = load_idx(pid + kProd);
         for (int c = pid; c < nchunks; c += kProd) {
             const int64_t e2 = load_idx(c + 2 * kProd);
