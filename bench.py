@@ -385,9 +385,10 @@ def our_arm(a, rank, world):
                       frac=kern[dom]["tflops"] / peak, traffic=traffic,
                       peak_source="measured FFMA probe (ndg_fp32_probe) on this GPU; MEASURED_PEAKS.json has no "
                                   "FP32 entry",
-                      bound_note="the dominant kernel (K7 backward) runs on the FP32 SIMT pipe: it reads ~2 GB/step "
-                                 "(far from the HBM roof) and issues no tensor-core work, so neither 'hbm' nor "
-                                 "'tensor' applies; the K5 forward's tensor roofline is in kernels.forward",
+                      bound_note="the dominant kernel (K7 backward) runs on the FP32 SIMT pipe: its DRAM traffic "
+                                 "(`traffic`, mostly float64 atomic write-backs) is ~7% of the HBM roof and it issues "
+                                 "no tensor-core work, so neither 'hbm' nor 'tensor' applies; the K5 forward's "
+                                 "tensor roofline is in kernels.forward",
                       peak_nominal=NOMINAL_FP32_TFLOPS, frac_of_nominal=kern[dom]["tflops"] / NOMINAL_FP32_TFLOPS,
                       flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n)),
                       step_achieved=step_tflops, step_frac=step_tflops / peak),
