@@ -179,6 +179,17 @@ int ndg_active_mask(int n, int64_t B, int tile, const float* queries, const doub
                     void* stream);
 
 /*
+ * Diagnostic for cmd_gradcheck: the rel-L2 loss of M raw-parameter variants
+ * (params / child: float64 [M][G][N+P+4], flags [G]) at B queries in float64, culling off. With
+ * inv_den = NULL the kernel writes variant 0's prediction to pred_out[B][3] (the base pass); with
+ * inv_den = 1 / (pred_base^2 + eps) [B][3] it writes loss[m] (the denominator held at the base
+ * prediction, as the finite differences of SPEC.md:273-281 with a detached denominator require).
+ */
+int ndg_loss_f64(int n, int G, int amp_mode, int M, const double* params, const double* child, const uint8_t* flags,
+                 int64_t B, const float* queries, const float* targets, const double* inv_den, double* pred_out,
+                 double* loss, void* stream);
+
+/*
  * K8 epilogue. Replaces the tail of `backward`: raw-parameter gradients of parents
  * and live children including the child->parent cross terms; stats[Gev][3] =
  * (loss share, gradient proxy, pairs). Non-finite gradients -> status NONFINITE_GRADIENT.

@@ -3,6 +3,7 @@
     ndgauss fit  --config PATH --out DIR [--resume CKPT]
     ndgauss eval --ckpt PATH (--queries PATH | --grid SPEC) --out DIR [--ref PATH] [--no-cull]
     ndgauss bench-cull --config PATH --out CSV
+    ndgauss gradcheck [--seed S]
 
 fit writes metrics.csv (iteration,loss,n_components,culled_fraction,ms_per_iter) and a checkpoint
 every phase and at the end; exit 0 on completion, 2 on a config error, 3 on TrainingAborted
@@ -17,7 +18,8 @@ the wall-clock of culled vs brute-force evaluation. Multiplier >= 3 rows have no
 Cauchy-Schwarz; multiplier 1 rows show the paper's artifact regime. (The culled tail still moves pred
 by up to exp(-m^2/2) * sum |a| of the dropped Gaussians, so max_abs_err is reported, not bounded by
 1e-6: DESIGN.md §5.)
-`gradcheck` is not provided.
+gradcheck compares the analytic gradients with central finite differences of a
+float64 evaluator (paper_2405_20067_b200/gradcheck.py); exit 0 iff the max relative error < 1e-4.
 """
 from __future__ import annotations
 
@@ -242,6 +244,11 @@ def cmd_bench_cull(args) -> int:
     return 0
 
 
+def cmd_gradcheck(args) -> int:
+    from . import gradcheck
+    return 0 if gradcheck.run(seed=args.seed, per_n=args.per_n) else 1
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="ndgauss")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -260,9 +267,13 @@ def main(argv=None) -> int:
     bc = sub.add_parser("bench-cull")
     bc.add_argument("--config", required=True)
     bc.add_argument("--out", required=True)
+    gc = sub.add_parser("gradcheck")
+    gc.add_argument("--seed", type=int, default=0)
+    gc.add_argument("--per-n", type=int, default=100, help="random mixtures per (N, amplitude mode)")
     args = ap.parse_args(argv)
     try:
-        return {"fit": cmd_fit, "eval": cmd_eval, "bench-cull": cmd_bench_cull}[args.cmd](args)
+        return {"fit": cmd_fit, "eval": cmd_eval, "bench-cull": cmd_bench_cull,
+                "gradcheck": cmd_gradcheck}[args.cmd](args)
     except NdgError as err:
         print(f"error: {err}", file=sys.stderr)
         return 1

@@ -72,6 +72,122 @@ int launch_active(int64_t T, int tile, const float* q, const double* mean64, con
     return NDG_OK;
 }
 
+// ------------------------------------------------------------------------------------------------
+// gradcheck support (cmd_gradcheck): the rel-L2 loss of M raw-parameter variants in
+// float64, culling off. CTA = variant: its threads activate the variant's evaluated Gaussians exactly
+// as K1 does (diagonal exp, off-diagonal 2 sigmoid - 1, child composition m_c = L m_u + m_p, L U,
+// alpha * sigmoid(colour)) into shared memory, then sweep the queries (forward substitution in
+// float64) and reduce sum_q,ch (p - t)^2 * inv_den[q, ch] / (3B). inv_den = 1 / (pbar^2 + eps) is the
+// detached denominator held at the base prediction (oracle pin 4); with inv_den == NULL the kernel
+// instead writes variant 0's prediction to pred_out (the base pass).
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ double gc_offdiag(double r) { return 2.0 / (1.0 + exp(-r)) - 1.0; }
+__device__ __forceinline__ double gc_sigmoid(double r) { return 1.0 / (1.0 + exp(-r)); }
+
+template <int N>
+__global__ void loss_f64_kernel(int G, int amp_mode, const double* __restrict__ params, const double* __restrict__ child,
+                                const uint8_t* __restrict__ flags, int64_t B, const float* __restrict__ queries,
+                                const float* __restrict__ targets, const double* __restrict__ inv_den,
+                                double* __restrict__ pred_out, double* __restrict__ loss_out) {
+    constexpr int P = n_chol(N), R = raw_floats(N), W = P + N + 3;   // per evaluated Gaussian: L | m | a
+    extern __shared__ double s_g[];                                     // [2G][W]
+    __shared__ double s_red[256];
+    const int m = blockIdx.x, tid = threadIdx.x;
+    const double* pv = params + (int64_t)m * G * R;
+    const double* cv = child + (int64_t)m * G * R;
+    for (int e = tid; e < 2 * G; e += blockDim.x) {
+        const bool is_child = e >= G;
+        const int i = is_child ? e - G : e;
+        const uint8_t f = flags[i];
+        double* out = s_g + e * W;
+        const bool live = !(f & 2) && (!is_child || (f & 1));
+        double L[P], mu[N];
+        for (int r = 0; r < N; ++r)
+            for (int c = 0; c <= r; ++c) {
+                const double raw = pv[i * R + N + tri(r, c)];
+                L[tri(r, c)] = r == c ? exp(raw) : gc_offdiag(raw);
+            }
+        for (int r = 0; r < N; ++r) mu[r] = pv[i * R + r];
+        const double* arow = pv + i * R;
+        if (is_child) {
+            double U[P], Lc[P], mc[N];
+            const double* crow = cv + i * R;
+            for (int r = 0; r < N; ++r)
+                for (int c = 0; c <= r; ++c) {
+                    const double raw = crow[N + tri(r, c)];
+                    U[tri(r, c)] = r == c ? exp(raw) : gc_offdiag(raw);
+                }
+            for (int r = 0; r < N; ++r) {
+                double acc = mu[r];
+                for (int k = 0; k <= r; ++k) acc += L[tri(r, k)] * crow[k];
+                mc[r] = acc;
+            }
+            for (int r = 0; r < N; ++r)
+                for (int c = 0; c <= r; ++c) {
+                    double acc = 0.0;
+                    for (int k = c; k <= r; ++k) acc += L[tri(r, k)] * U[tri(k, c)];
+                    Lc[tri(r, c)] = acc;
+                }
+            for (int t = 0; t < P; ++t) L[t] = Lc[t];
+            for (int r = 0; r < N; ++r) mu[r] = mc[r];
+            arow = crow;
+        }
+        const double ampr = arow[N + P + 3];
+        const double alpha = amp_mode == NDG_BRIGHTNESS ? exp(ampr) : gc_sigmoid(ampr);
+        for (int t = 0; t < P; ++t) out[t] = L[t];
+        for (int r = 0; r < N; ++r) out[P + r] = mu[r];
+        for (int ch = 0; ch < 3; ++ch) out[P + N + ch] = live ? alpha * gc_sigmoid(arow[N + P + ch]) : 0.0;
+    }
+    __syncthreads();
+    double acc = 0.0;
+    for (int64_t q = tid; q < B; q += blockDim.x) {
+        double x[N], p[3] = {0.0, 0.0, 0.0};
+        for (int d = 0; d < N; ++d) x[d] = (double)queries[q * N + d];
+        for (int e = 0; e < 2 * G; ++e) {
+            const double* ge = s_g + e * W;
+            if (ge[P + N] == 0.0 && ge[P + N + 1] == 0.0 && ge[P + N + 2] == 0.0) continue;
+            double z[N], s2 = 0.0;
+            for (int r = 0; r < N; ++r) {
+                double a = x[r] - ge[P + r];
+                for (int k = 0; k < r; ++k) a -= ge[tri(r, k)] * z[k];
+                z[r] = a / ge[tri(r, r)];
+                s2 += z[r] * z[r];
+            }
+            const double g = exp(-0.5 * s2);
+            for (int ch = 0; ch < 3; ++ch) p[ch] += g * ge[P + N + ch];
+        }
+        if (inv_den) {
+            for (int ch = 0; ch < 3; ++ch) {
+                const double d = p[ch] - (double)targets[q * 3 + ch];
+                acc += d * d * inv_den[q * 3 + ch];
+            }
+        } else if (m == 0 && pred_out) {
+            for (int ch = 0; ch < 3; ++ch) pred_out[q * 3 + ch] = p[ch];
+        }
+    }
+    s_red[tid] = acc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (tid < o) s_red[tid] += s_red[tid + o];
+        __syncthreads();
+    }
+    if (tid == 0) loss_out[m] = s_red[0] / (3.0 * (double)B);
+}
+
+template <int N>
+int launch_loss_f64(int G, int amp_mode, int M, const double* params, const double* child, const uint8_t* flags,
+                    int64_t B, const float* q, const float* t, const double* inv_den, double* pred_out, double* loss,
+                    cudaStream_t st) {
+    constexpr int W = n_chol(N) + N + 3;
+    const size_t smem = sizeof(double) * 2 * (size_t)G * W;
+    NDG_REQUIRE(smem <= 160 * 1024, "too many components for the float64 gradcheck evaluator");
+    static DeviceOnce attr;
+    if (attr.first()) cudaFuncSetAttribute(loss_f64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    loss_f64_kernel<N><<<M, 256, smem, st>>>(G, amp_mode, params, child, flags, B, q, t, inv_den, pred_out, loss);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
 }  // namespace
 
 extern "C" int ndg_active_mask(int n, int64_t B, int tile, const float* queries, const double* mean64,
@@ -85,6 +201,24 @@ extern "C" int ndg_active_mask(int n, int64_t B, int tile, const float* queries,
 #define NDG_CASE(NN) \
     case NN:         \
         return launch_active<NN>(T, tile, queries, mean64, chol64, eflags, Gev, max_s2, mask, counts, st);
+        NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
+        NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
+#undef NDG_CASE
+        default:
+            return NDG_ERR_UNSUPPORTED_DIMS;
+    }
+}
+
+extern "C" int ndg_loss_f64(int n, int G, int amp_mode, int M, const double* params, const double* child,
+                            const uint8_t* flags, int64_t B, const float* queries, const float* targets,
+                            const double* inv_den, double* pred_out, double* loss, void* stream) {
+    NDG_REQUIRE(G >= 1 && M >= 1 && B >= 1, "need at least one component, variant and query");
+    NDG_REQUIRE(inv_den || pred_out, "the base pass (inv_den == NULL) needs pred_out");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    switch (n) {
+#define NDG_CASE(NN) \
+    case NN:         \
+        return launch_loss_f64<NN>(G, amp_mode, M, params, child, flags, B, queries, targets, inv_den, pred_out, loss, st);
         NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
         NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
 #undef NDG_CASE

@@ -44,6 +44,7 @@ SIGNATURES = {
     "ndg_backward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _P],
     "ndg_moments_to_zspace": [_I, _L, _P, _P, _P, _P, _P],
     "ndg_active_mask": [_I, _L, _I, _P, _P, _P, _P, _L, _D, _P, _P, _P],
+    "ndg_loss_f64": [_I, _I, _I, _I, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P],
     "ndg_epilogue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "ndg_adam": [_I, _L, _P, _P, _P, _P, _P, _I, _F, _F, _F, _F, _F, _F, _F, _P],
     "ndg_tc_records": [_I, _L, _P, _P, _P, _P, _P, _P, _P],
@@ -90,7 +91,7 @@ class NdgLaunchError(RuntimeError):
 # entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
 LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_scan_counts",
              "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_backward", "ndg_backward_tc",
-             "ndg_moments_to_zspace", "ndg_active_mask", "ndg_centre_records", "ndg_epilogue", "ndg_adam",
+             "ndg_moments_to_zspace", "ndg_active_mask", "ndg_centre_records", "ndg_loss_f64", "ndg_epilogue", "ndg_adam",
              "ndg_fp32_probe", "ndg_tf32_probe"}
 launch_count = 0
 

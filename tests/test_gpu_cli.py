@@ -69,3 +69,12 @@ def test_bench_cull_ablation(cuda, tmp_path):
             kept = {int(r["k"]): int(r["kept_pairs"]) for r in rows
                     if r["tile_size"] == tile and float(r["multiplier"]) == float(m)}
             assert kept[16] <= kept[4]
+
+
+def test_gradcheck_command(cuda):
+    """cmd_gradcheck: passes on random mixtures with live children across N and both
+    amplitude modes (reduced count here; the full default run takes ~8 s), and the negative control
+    (a corrupted analytic coordinate) fails."""
+    from paper_2405_20067_b200 import cli, gradcheck
+    assert cli.main(["gradcheck", "--seed", "3", "--per-n", "4"]) == 0
+    assert not gradcheck.run(seed=3, per_n=1, dims=(4,), corrupt=True, out=lambda *_: None)
