@@ -309,3 +309,27 @@ def test_tc_forward_sharp_gaussians(cuda, sigma0, regime, want_tc):
     assert np.array_equal(res.candidates.idx.cpu().numpy(), ref["idx"])
     assert _rel(res.pred.cpu().numpy(), ref["pred"]) < RTOL
     _check_grads(10, res.grads.params.cpu().numpy(), ref["grad_parent"], "parent")
+
+
+@pytest.mark.parametrize("N,amp_mode", [(1, 0), (4, 1), (10, 0)])
+def test_loss_f64_evaluator_vs_oracle(cuda, N, amp_mode):
+    """ndg_loss_f64 (gradcheck's finite-difference evaluator) is the float64 model itself: its base
+    prediction and its loss with the base denominator match the oracle (culling off) to ~1e-12."""
+    from paper_2405_20067_b200 import kernels as K
+    om, mix, q, t = _mk(N, 6, 256, children=True, amp_mode=amp_mode, sigma0=0.2)
+    ref = O.fwd_bwd(om, q, t, O.make_projection_set(N, 16, 0), tile_size=256, cull=False)
+    dev = torch.device("cuda", 0)
+    base = torch.from_numpy(np.concatenate([om.params, om.child]).astype(np.float64)).to(dev)
+    par, chi = base[:6].contiguous(), base[6:].contiguous()
+    qd, td = torch.from_numpy(q).to(dev), torch.from_numpy(t).to(dev)
+    pred = torch.empty(256, 3, dtype=torch.float64, device=dev)
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    K.call("ndg_loss_f64", N, 6, amp_mode, 1, par.data_ptr(), chi.data_ptr(), mix.flags.data_ptr(), 256,
+           qd.data_ptr(), td.data_ptr(), None, pred.data_ptr(), loss.data_ptr(), s)
+    p = pred.cpu().numpy()
+    assert np.abs(p - ref["pred"]).max() <= 1e-12 * max(1.0, np.abs(ref["pred"]).max())
+    inv = (1.0 / (pred * pred + 0.01)).contiguous()
+    K.call("ndg_loss_f64", N, 6, amp_mode, 1, par.data_ptr(), chi.data_ptr(), mix.flags.data_ptr(), 256,
+           qd.data_ptr(), td.data_ptr(), inv.data_ptr(), None, loss.data_ptr(), s)
+    assert abs(float(loss.cpu()[0]) - ref["loss"]) <= 1e-12 * abs(ref["loss"])
