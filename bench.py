@@ -26,7 +26,6 @@ import os
 import statistics
 import subprocess
 import sys
-import tempfile
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -157,25 +156,53 @@ class ClockSampler:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
+    """nvidia-smi polling every 100 ms, started BEFORE the warm-up: its NVML start-up stalls the driver for
+    tens of ms, which inflated short host-latency-bound timed regions when it was launched inside them.
+    Rows are stamped on arrival; stop() keeps those that arrived inside [begin(), end()] (or, for a timed
+    region shorter than the poll period, the first row after begin())."""
+
     def __init__(self, gpu_index):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        import threading
+        self.rows, self.t0, self.t1 = [], None, None
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-i", str(gpu_index), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-i", str(gpu_index), "-lms", "100"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+        deadline = time.monotonic() + 10.0
+        while not self.rows and time.monotonic() < deadline and self.p.poll() is None:
+            time.sleep(0.02)                      # wait until NVML is up and sampling
+
+    def _read(self):
+        for line in self.p.stdout:
+            if line.count(",") >= 8:
+                self.rows.append((time.monotonic(), line.strip().split(",")))
+
+    def begin(self):
+        self.t0 = time.monotonic()
+
+    def end(self):
+        self.t1 = time.monotonic()
 
     def stop(self):
         if self.p is None:
             return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"])
+        if self.t1 is not None and not any(t >= self.t0 for t, _ in self.rows):
+            time.sleep(0.25)                      # region shorter than the poll period: take the next row
         self.p.terminate()
         try:
             self.p.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.p.kill()
-        self.f.flush()
-        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 8]
-        os.unlink(self.f.name)
+        self.th.join(timeout=5)
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = self.t1 if self.t1 is not None else float("inf")
+        inside = [r for t, r in self.rows if t0 <= t <= t1]
+        rows = inside or [r for t, r in self.rows if t >= t0][:1]
         if not rows:
             return dict(sm_mhz=None, sm_max_mhz=None, reasons=["no samples"])
         sm = [float(r[1]) for r in rows]
@@ -249,18 +276,20 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
         ndg.adam_step(mix, grads, state, step=it[0])
         return res
 
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) if rank == 0 else None
     for _ in range(warmup):
         res = step(qd, td)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) if rank == 0 else None
     hp.enable_kernel_timing(True)
     launches0 = K.launch_count
     step_ms, kept, pairs = [], [], []
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    if clocks:
+        clocks.begin()
     for _ in range(steps):
         flush.zero_()                                   # L2 flush, outside the timed interval
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -272,6 +301,8 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
         kept.append(res.kept_fraction)
         pairs.append(res.candidates.n_pairs_tiles * a.tile)
     torch.cuda.synchronize()
+    if clocks:
+        clocks.end()
     if world > 1:
         dist.barrier()
     launches = K.launch_count - launches0
