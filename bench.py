@@ -253,6 +253,24 @@ def tf32_peak(torch, K, dev):
     return best
 
 
+def hmma_peak(torch, K, dev):
+    """Measured mma.sync m16n8k8 tf32 rate (TFLOP/s) -- the tensor roofline of the warp-MMA K7."""
+    import ctypes
+    out = torch.empty(512, device=dev)
+    s = torch.cuda.current_stream()
+    blocks, iters = 148, 4000
+    K.call("ndg_hmma_probe", ctypes.c_void_p(out.data_ptr()), blocks, iters, ctypes.c_void_p(s.cuda_stream))
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        K.call("ndg_hmma_probe", ctypes.c_void_p(out.data_ptr()), blocks, iters, ctypes.c_void_p(s.cuda_stream))
+        b.record()
+        b.synchronize()
+        best = max(best, K.load().ndg_hmma_probe_flops(blocks, iters) / (a.elapsed_time(b) * 1e-3) / 1e12)
+    return best
+
+
 def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmup, measure_e2e):
     import numpy as np
 
@@ -394,6 +412,14 @@ def our_arm(a, rank, world):
         t_tf = pairs * tc_f / (main["fwd_ms"] * 1e-3) / 1e12
         kern["forward"].update(impl="tcgen05 kind::tf32 (3xTF32)", tensor_tflops=t_tf, tensor_peak_measured=tpeak,
                                frac_of_measured_tf32=t_tf / tpeak, tensor_flops_per_pair=tc_f)
+    if main["bwd_impl"] == "mma":
+        # warp-MMA K7: per 8 queries of one Gaussian, 12 m16n8k8 MMAs (z-GEMM 2 k-steps x 3, S-GEMM
+        # 2 n-blocks x 3) = 3072 tensor flops per pair on the padded 16-dim block
+        hpeak = hmma_peak(torch, K, dev)
+        mm_f = 12 * 2 * 16 * 8 * 8 // 8
+        m_tf = pairs * mm_f / (main["bwd_ms"] * 1e-3) / 1e12
+        kern["backward"].update(impl="mma.sync m16n8k8 tf32 (3xTF32)", tensor_tflops=m_tf, tensor_peak_measured=hpeak,
+                                frac_of_measured_hmma=m_tf / hpeak, tensor_flops_per_pair=mm_f)
     dom = max(kern, key=lambda k: kern[k]["ms"])
     traffic = None
     try:
@@ -412,7 +438,18 @@ def our_arm(a, rank, world):
                     kept_fraction=main["kept"], pairs_per_step=pairs, sigma0=main["sigma0"],
                     l2="flushed before every timed step (256 MiB write, outside the timed interval)",
                     parallelism=f"dp{world} (tiles sharded, mixture replicated, 1 NCCL allreduce/step)"),
-        roofline=dict(bound="fp32", kernel=dom, achieved=kern[dom]["tflops"], peak=peak, unit="TFLOP/s",
+        roofline=(dict(bound="tensor", kernel=dom, achieved=kern[dom]["tensor_tflops"],
+                       peak=kern[dom]["tensor_peak_measured"], unit="TFLOP/s",
+                       frac=kern[dom]["frac_of_measured_hmma"], traffic=traffic,
+                       peak_source="measured mma.sync m16n8k8 tf32 probe (ndg_hmma_probe) on this GPU: the legacy "
+                                   "warp-level tensor path this kernel issues, not the tcgen05 peak",
+                       bound_note="the dominant kernel is the warp-MMA K7 (N = 16): achieved counts its padded "
+                                  "3xTF32 MMA flops (3072 per pair); its FP32-equivalent rate is in kernels.backward",
+                       flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n),
+                                           backward_tensor=kern[dom]["tensor_flops_per_pair"]),
+                       step_achieved=step_tflops, step_frac=step_tflops / peak)
+                  if dom == "backward" and main["bwd_impl"] == "mma" else
+                  dict(bound="fp32", kernel=dom, achieved=kern[dom]["tflops"], peak=peak, unit="TFLOP/s",
                       frac=kern[dom]["tflops"] / peak, traffic=traffic,
                       peak_source="measured FFMA probe (ndg_fp32_probe) on this GPU; MEASURED_PEAKS.json has no "
                                   "FP32 entry",
@@ -422,7 +459,7 @@ def our_arm(a, rank, world):
                                  "tensor roofline is in kernels.forward",
                       peak_nominal=NOMINAL_FP32_TFLOPS, frac_of_nominal=kern[dom]["tflops"] / NOMINAL_FP32_TFLOPS,
                       flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n)),
-                      step_achieved=step_tflops, step_frac=step_tflops / peak),
+                      step_achieved=step_tflops, step_frac=step_tflops / peak)),
         kernels=kern, gpu_launches=main["launches"], clocks=main["clocks"], loss=main["loss"],
     )
     if "e2e" in main:

@@ -79,3 +79,32 @@ extern "C" int ndg_tf32_probe(float* out, int blocks, int iters, void* stream) {
 }
 
 extern "C" double ndg_tf32_probe_flops(int blocks, int iters) { return 2.0 * 128 * 256 * 8 * (double)iters * blocks; }
+
+// Warp-level tensor-core peak probe (mma.sync m16n8k8 tf32, the K7-MMA instruction): 512 threads per
+// CTA, each warp running 8 independent accumulator chains -- the roofline denominator for K7-MMA.
+__global__ void __launch_bounds__(512) hmma_probe_kernel(int iters, float* out) {
+    float d[8][4] = {};
+    uint32_t a[4], b[2];
+    for (int i = 0; i < 4; ++i) a[i] = __float_as_uint(1.0f + threadIdx.x * 1e-3f + i);
+    for (int i = 0; i < 2; ++i) b[i] = __float_as_uint(0.5f + i);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+                         "{%8,%9}, {%0,%1,%2,%3};\n"
+                         : "+f"(d[k][0]), "+f"(d[k][1]), "+f"(d[k][2]), "+f"(d[k][3])
+                         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+    }
+    float s = 0.f;
+    for (int k = 0; k < 8; ++k) s += d[k][0] + d[k][1] + d[k][2] + d[k][3];
+    if (s == 12345.f) out[threadIdx.x] = s;
+}
+
+extern "C" int ndg_hmma_probe(float* out, int blocks, int iters, void* stream) {
+    NDG_REQUIRE(blocks >= 1 && iters >= 1, "blocks and iters must be positive");
+    hmma_probe_kernel<<<blocks, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(iters, out);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+extern "C" double ndg_hmma_probe_flops(int blocks, int iters) { return 2.0 * 16 * 8 * 8 * 8 * 16 * (double)iters * blocks; }

@@ -7,10 +7,12 @@ gmm-core, culling and grad modules, each enqueued on the current CUDA stream thr
     K2 ndg_project       project_components
     K3 ndg_tile_bounds   TileBounds
     K4 ndg_cull_*        cull_tile for every tile -> CSR candidate lists
-    K5 ndg_forward       eval_mixture (+ K6 loss_rel_l2 fused)
-    K7 ndg_backward_tc   backward pair loop on tcgen05 (z-GEMM + moments)
-       ndg_backward      (FP32-pipe pair loop: N > 12 or NDG_BACKWARD=fp32)
-    K7b ndg_moments_to_zspace  x-space moments -> S', t' (tensor-core K7 only)
+    K5 ndg_forward_tc    eval_mixture (+ K6 loss_rel_l2 fused), tcgen05
+       ndg_forward       (FP32-pipe K5: ill-conditioned mixtures, tiles > 256, NDG_FORWARD=fp32)
+    K7 ndg_backward      backward pair loop, FP32 pipe (N <= 15)
+       ndg_backward_mma  (warp-MMA pair loop: N = 16, or NDG_BACKWARD=mma for N >= 9)
+       ndg_backward_tc   (opt-in NDG_BACKWARD=tc: tcgen05 z-GEMM + moments, N <= 12)
+    K7b ndg_moments_to_zspace  x-space moments -> S', t' (tcgen05 K7 only)
     K8 ndg_epilogue      backward tail, raw-parameter chain rule
     K9 ndg_adam          adam_step
 
@@ -205,12 +207,20 @@ class HotPath:
             raise ValueError("forward must be 'tc' or 'fp32'")
         if self.forward_impl == "tc" and self.tile > 256:
             self.forward_impl = "fp32"      # the tcgen05 K5 covers tiles of up to two 128-query halves
-        # K7 implementation: "fp32" = FP32-pipe pair loop (default); "tc" = tcgen05 z-GEMM + moments GEMM
+        # K7 implementation: "auto" (default) = warp-MMA K7 for N >= MMA_MIN_N, else the FP32-pipe pair
+        # loop; "fp32" / "mma" force one (both per-step guarded); "tc" = tcgen05 z-GEMM + moments GEMM
         # (N <= 12, opt-in: no faster and only marginally within 1e-4)
-        bwd = backward or os.environ.get("NDG_BACKWARD", "fp32")
-        if bwd not in ("tc", "fp32"):
-            raise ValueError("backward must be 'tc' or 'fp32'")
-        self.backward_impl = "tc" if bwd == "tc" and K.load().ndg_backward_tc_supported(self.n) else "fp32"
+        bwd = backward or os.environ.get("NDG_BACKWARD", "auto")
+        if bwd not in ("auto", "tc", "fp32", "mma"):
+            raise ValueError("backward must be 'auto', 'fp32', 'mma' or 'tc'")
+        lib = K.load()
+        if bwd == "tc":
+            bwd = "tc" if lib.ndg_backward_tc_supported(self.n) else "fp32"
+        elif bwd == "auto":
+            bwd = "mma" if self.n >= self.MMA_MIN_N else "fp32"
+        if bwd == "mma" and not (lib.ndg_backward_mma_supported(self.n) and self.tile % 8 == 0):
+            bwd = "fp32"
+        self.backward_impl = bwd
         self._recs = None    # the last activation: its conditioning bound rides on the cull's read-back
         self.last_forward_impl = self.last_backward_impl = None   # what the last step ran
         self.last_centred = False
@@ -284,6 +294,22 @@ class HotPath:
     def backward_tc_ok(self, recs: EvalRecords) -> bool:
         return (self.backward_impl == "tc" and recs.rec_tc is not None
                 and recs.tc_conditioning() <= self.TC_BACKWARD_MAX_BOUND)
+
+    # The warp-MMA K7 forms z~ with the K5 z-GEMM (same records, same error ~2e-7 * RMS(B)), so it
+    # shares the tensor-core forward's bound. Its cost does not depend on N (dims pad to one m16
+    # block); the FP32 K7's grows with N and spills from 13 on. Measured crossover (50k Gaussians,
+    # 2^18 queries): 122 vs 272 ms at N=13, 270 vs 269 at 15, 330 vs 266 at 16.
+    MMA_MIN_N = 16
+
+    def backward_mma_ok(self, recs: EvalRecords) -> bool:
+        return (self.backward_impl == "mma" and recs.rec_tc is not None
+                and recs.tc_conditioning() <= self.TC_FORWARD_MAX_BOUND)
+
+    def backward_kernel_impl(self, recs: EvalRecords) -> str:
+        """Which K7 this step runs: "tc", "mma" or "fp32"."""
+        if self.backward_tc_ok(recs):
+            return "tc"
+        return "mma" if self.backward_mma_ok(recs) else "fp32"
 
     # -- K2 --------------------------------------------------------------------------------
     def project(self, recs: EvalRecords) -> ProjectedBounds:
@@ -399,8 +425,12 @@ class HotPath:
         B = int(qrec.shape[0])
         accum = torch.zeros(recs.Gev, self.L["acc"], dtype=torch.float64, device=self.device)
         self._ev("backward", 0)
-        self.last_backward_impl = "tc" if self.backward_tc_ok(recs) else "fp32"
-        if self.last_backward_impl == "tc":
+        self.last_backward_impl = self.backward_kernel_impl(recs)
+        if self.last_backward_impl == "mma":
+            K.call("ndg_backward_mma", self.n, B, self.tile, _p(qrec), _p(recs.rec_tc), _p(cl.offsets), _p(cl.idx),
+                   _p(cl.chunk_offsets), cl.n_chunks, _p(accum), _stream())
+            self._ev("backward", 1)
+        elif self.last_backward_impl == "tc":
             K.call("ndg_backward_tc", self.n, B, self.tile, _p(qrec), _p(recs.rec_tc), _p(cl.offsets), _p(cl.idx),
                    _p(accum), _stream())
             self._ev("backward", 1)

@@ -43,6 +43,8 @@ SIGNATURES = {
     "ndg_backward_tc_supported": [_I],
     "ndg_backward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _P],
     "ndg_moments_to_zspace": [_I, _L, _P, _P, _P, _P, _P],
+    "ndg_backward_mma_supported": [_I],
+    "ndg_backward_mma": [_I, _L, _I, _P, _P, _P, _P, _P, _L, _P, _P],
     "ndg_active_mask": [_I, _L, _I, _P, _P, _P, _P, _L, _D, _P, _P, _P],
     "ndg_loss_f64": [_I, _I, _I, _I, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P],
     "ndg_epilogue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
@@ -53,6 +55,8 @@ SIGNATURES = {
     "ndg_fp32_probe_flops": [_I, _I],
     "ndg_tf32_probe": [_P, _I, _I, _P],
     "ndg_tf32_probe_flops": [_I, _I],
+    "ndg_hmma_probe": [_P, _I, _I, _P],
+    "ndg_hmma_probe_flops": [_I, _I],
 }
 
 ERRORS = {0: "NDG_OK", 1: "NDG_ERR_INVALID_PARAMETER", 2: "NDG_ERR_NONFINITE_GRADIENT",
@@ -79,7 +83,7 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = {"ndg_last_error": C.c_char_p, "ndg_fp32_probe_flops": C.c_double,
-                      "ndg_tf32_probe_flops": C.c_double}.get(name, C.c_int)
+                      "ndg_tf32_probe_flops": C.c_double, "ndg_hmma_probe_flops": C.c_double}.get(name, C.c_int)
     _lib = lib
     return lib
 
@@ -90,9 +94,9 @@ class NdgLaunchError(RuntimeError):
 
 # entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
 LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_scan_counts",
-             "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_backward", "ndg_backward_tc",
+             "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_backward", "ndg_backward_tc", "ndg_backward_mma",
              "ndg_moments_to_zspace", "ndg_active_mask", "ndg_centre_records", "ndg_loss_f64", "ndg_epilogue", "ndg_adam",
-             "ndg_fp32_probe", "ndg_tf32_probe"}
+             "ndg_fp32_probe", "ndg_tf32_probe", "ndg_hmma_probe"}
 launch_count = 0
 
 

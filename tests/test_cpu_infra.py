@@ -64,6 +64,8 @@ def test_abi_layout_queries():
         assert lib.ndg_accum_doubles(n) == O.n_chol(n) + n + 7
         # tensor-core backward: moments of (N+1)(N+2)/2 features must fit one M=128 GEMM and smem
         assert lib.ndg_backward_tc_supported(n) == (1 if n <= 12 else 0)
+        # warp-MMA backward: one m16 block of dims, only where the FP32 K7's registers run short
+        assert lib.ndg_backward_mma_supported(n) == (1 if 9 <= n <= 16 else 0)
     assert not lib.ndg_supported_dims(0) and not lib.ndg_supported_dims(17)
     assert lib.ndg_num_stats() == O.N_STATS
 

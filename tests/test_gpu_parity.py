@@ -154,6 +154,57 @@ def test_tc_backward_parity(cuda, N, G, B, children, regime, sigma0):
         assert _rel(st[:, j], ref["stats"][:, j]) < RTOL, f"stat {j}"
 
 
+@pytest.mark.parametrize("N,G,B,children,regime", [
+    (9, 300, 1024, True, "R"),
+    (11, 300, 1024, False, "C"),
+    (13, 300, 1024, True, "R"),
+    (14, 200, 512, False, "R"),
+    (15, 200, 1024, True, "C"),
+    (16, 300, 1024, True, "R"),
+    (16, 400, 2048, False, "C"),
+])
+def test_mma_backward_parity(cuda, N, G, B, children, regime):
+    """Warp-MMA K7 (ndg_backward_mma, the default at N = 16; forced here down to N = 9) against the float64 oracle, at the
+    default sigma0 (sharper than the tcgen05-moments cases above: z~ is formed in z-space)."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(N, G, B, children=children, regime=regime)
+    hp = ndg.HotPath(N, projection_seed=2, backward="mma")
+    assert hp.backward_impl == "mma"
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    assert hp.last_backward_impl == "mma"
+    ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
+    assert np.array_equal(res.candidates.idx.cpu().numpy(), ref["idx"])
+    _check_grads(N, res.grads.params.cpu().numpy(), ref["grad_parent"], "parent")
+    if children:
+        _check_grads(N, res.grads.child.cpu().numpy(), ref["grad_child"], "child")
+    st = res.grads.stats.cpu().numpy()
+    for j in range(3):
+        assert _rel(st[:, j], ref["stats"][:, j]) < RTOL, f"stat {j}"
+
+
+def test_mma_backward_selection(cuda):
+    """auto: FP32 K7 below MMA_MIN_N, warp-MMA K7 from it on; tiles not a multiple of 8 and
+    ill-conditioned steps (the z-GEMM bound) run the FP32 K7; the entry point refuses N < 9."""
+    ndg = _ndg()
+    from paper_2405_20067_b200 import kernels as K
+    M = ndg.HotPath.MMA_MIN_N
+    assert ndg.HotPath(M - 1).backward_impl == "fp32"
+    assert ndg.HotPath(M).backward_impl == "mma"
+    assert ndg.HotPath(16, tile_size=100).backward_impl == "fp32"
+    assert ndg.HotPath(16, backward="fp32").backward_impl == "fp32"
+    with pytest.raises(RuntimeError):
+        K.call("ndg_backward_mma", 8, 256, 256, 0, 0, 0, 0, 0, 1, 0, 0)
+    # a sharp mixture: conditioning past TC_FORWARD_MAX_BOUND -> this step's K7 is the FP32 one
+    om, mix, q, t = _mk(16, 64, 512, sigma0=0.002)
+    hp = ndg.HotPath(16, projection_seed=2)
+    assert hp.backward_impl == "mma"
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    assert hp.activate(mix).tc_conditioning() > hp.TC_FORWARD_MAX_BOUND
+    assert hp.last_backward_impl == "fp32"
+    ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
+    _check_grads(16, res.grads.params.cpu().numpy(), ref["grad_parent"], "parent")
+
+
 def test_tc_backward_unsupported_dims_fall_back(cuda):
     """N > 12 has no tensor-core K7 (the moments do not fit one M=128 GEMM + shared memory): the
     engine selects the FP32 K7, and the raw entry point refuses loudly."""

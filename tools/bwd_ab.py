@@ -1,5 +1,6 @@
-"""A/B of the two K7 implementations on one workload: block-relative gradient differences between
-backward="tc" and backward="fp32" (same forward), plus K7 timings. Tuning aid, not a test."""
+"""A/B of two K7 implementations on one workload: block-relative gradient differences between
+backward=<--other> ("mma" or "tc") and backward="fp32" (same forward), plus K7 timings.
+Tuning aid, not a test."""
 import argparse, json, os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -15,6 +16,7 @@ ap.add_argument("--batch", type=int, default=1 << 16)
 ap.add_argument("--regime", default="R")
 ap.add_argument("--sigma0", type=float, default=None)
 ap.add_argument("--iters", type=int, default=2)
+ap.add_argument("--other", choices=["mma", "tc"], default="tc")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 kw = {} if a.sigma0 is None else dict(sigma0=a.sigma0)
@@ -24,7 +26,7 @@ t = D.synthetic_targets(a.batch, seed=3)
 mix = ndg.Mixture.from_arrays(a.n_dims, 0, **mix_np)
 qd, td = torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda()
 out = {}
-for impl in ("fp32", "tc"):
+for impl in ("fp32", a.other):
     hp = ndg.HotPath(a.n_dims, projection_seed=2, backward=impl)
     res = hp.fwd_bwd(mix, qd, td, check=False)
     hp.enable_kernel_timing(True)
@@ -37,7 +39,8 @@ n = a.n_dims
 blocks = dict(mean=slice(0, n), chol=slice(n, n + n_chol(n)), color=slice(n + n_chol(n), n + n_chol(n) + 3),
               amp=slice(n + n_chol(n) + 3, n + n_chol(n) + 4))
 rel = lambda x, y: float(np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300))
-errs = {k: rel(out["tc"]["g"][:, s], out["fp32"]["g"][:, s]) for k, s in blocks.items()}
-errs.update({f"stat{j}": rel(out["tc"]["st"][:, j], out["fp32"]["st"][:, j]) for j in range(3)})
-print(json.dumps(dict(n=n, G=a.gaussians, B=a.batch, regime=a.regime, impl_tc=out["tc"]["impl"],
-                      fp32_ms=out["fp32"]["ms"], tc_ms=out["tc"]["ms"], rel=errs)))
+o = a.other
+errs = {k: rel(out[o]["g"][:, s], out["fp32"]["g"][:, s]) for k, s in blocks.items()}
+errs.update({f"stat{j}": rel(out[o]["st"][:, j], out["fp32"]["st"][:, j]) for j in range(3)})
+print(json.dumps({"n": n, "G": a.gaussians, "B": a.batch, "regime": a.regime, f"impl_{o}": out[o]["impl"],
+                  "fp32_ms": out["fp32"]["ms"], f"{o}_ms": out[o]["ms"], "rel": errs}))
