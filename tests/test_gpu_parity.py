@@ -182,6 +182,22 @@ def test_mma_backward_parity(cuda, N, G, B, children, regime):
         assert _rel(st[:, j], ref["stats"][:, j]) < RTOL, f"stat {j}"
 
 
+@pytest.mark.parametrize("tile,amp_mode", [(8, 0), (64, 1), (512, 0), (1024, 1)])
+def test_mma_backward_tile_sizes(cuda, tile, amp_mode):
+    """K7-MMA's per-work-item x-hat fragments scale with the tile (tile * 144 B of shared memory):
+    the smallest (8 = one MMA column block) to the largest (1024) tile, both amplitude modes."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(16, 200, 2048, children=True, amp_mode=amp_mode)
+    hp = ndg.HotPath(16, projection_seed=2, tile_size=tile, forward="fp32")
+    assert hp.backward_impl == "mma"
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    assert hp.last_backward_impl == "mma"
+    ref = O.fwd_bwd(om, q, t, hp.ps.vectors, tile_size=tile)
+    assert np.array_equal(res.candidates.idx.cpu().numpy(), ref["idx"])
+    _check_grads(16, res.grads.params.cpu().numpy(), ref["grad_parent"], "parent")
+    _check_grads(16, res.grads.child.cpu().numpy(), ref["grad_child"], "child")
+
+
 def test_mma_backward_selection(cuda):
     """auto: FP32 K7 below MMA_MIN_N, warp-MMA K7 from it on; tiles not a multiple of 8 and
     ill-conditioned steps (the z-GEMM bound) run the FP32 K7; the entry point refuses N < 9."""
