@@ -413,10 +413,11 @@ def our_arm(a, rank, world):
         kern["forward"].update(impl="tcgen05 kind::tf32 (3xTF32)", tensor_tflops=t_tf, tensor_peak_measured=tpeak,
                                frac_of_measured_tf32=t_tf / tpeak, tensor_flops_per_pair=tc_f)
     if main["bwd_impl"] == "mma":
-        # warp-MMA K7: per 8 queries of one Gaussian, 12 m16n8k8 MMAs (z-GEMM 2 k-steps x 3, S-GEMM
-        # 2 n-blocks x 3) = 3072 tensor flops per pair on the padded 16-dim block
+        # warp-MMA K7: per 8 queries of one Gaussian, 8.5 m16n8k8 MMAs issued (z-GEMM: 3 for dims
+        # 0..7 + half of the 3 packed dims-8..15 ones; S-GEMM: 2 column blocks x 2) = 2176 tensor
+        # flops per pair on the padded 16-dim block
         hpeak = hmma_peak(torch, K, dev)
-        mm_f = 12 * 2 * 16 * 8 * 8 // 8
+        mm_f = 17 * 2 * 16 * 8 * 8 // (2 * 8)
         m_tf = pairs * mm_f / (main["bwd_ms"] * 1e-3) / 1e12
         kern["backward"].update(impl="mma.sync m16n8k8 tf32 (3xTF32)", tensor_tflops=m_tf, tensor_peak_measured=hpeak,
                                 frac_of_measured_hmma=m_tf / hpeak, tensor_flops_per_pair=mm_f)
@@ -443,8 +444,8 @@ def our_arm(a, rank, world):
                        frac=kern[dom]["frac_of_measured_hmma"], traffic=traffic,
                        peak_source="measured mma.sync m16n8k8 tf32 probe (ndg_hmma_probe) on this GPU: the legacy "
                                    "warp-level tensor path this kernel issues, not the tcgen05 peak",
-                       bound_note="the dominant kernel is the warp-MMA K7 (N = 16): achieved counts its padded "
-                                  "3xTF32 MMA flops (3072 per pair); its FP32-equivalent rate is in kernels.backward",
+                       bound_note="the dominant kernel is the warp-MMA K7 (N >= 15): achieved counts its padded "
+                                  "3xTF32 MMA flops (2176 per pair); its FP32-equivalent rate is in kernels.backward",
                        flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n),
                                            backward_tensor=kern[dom]["tensor_flops_per_pair"]),
                        step_achieved=step_tflops, step_frac=step_tflops / peak)

@@ -12,11 +12,14 @@
 // runs at a third of the FP32 peak. Here a warp owns a Gaussian and the 16 x 8 (dims x queries)
 // block of z~ is one MMA:
 //   MMA1  Z^T (16 x 8)  = Ahat (16 x 16) . Xhat^T (16 x 8),  C initialised to the bias column
-//   MMA2  S'  (16 x 16) += (w Z)^T-block (16 x 8) . Z (8 x 16)
+//   MMA2  S'  (16 x 16) += (s V)^T-block (16 x 8) . V (8 x 16),  V = sqrt|w| Z, s = sign w
 // MMA1's C fragment (lane (gid, tig): dims gid, gid+8 of queries 2tig, 2tig+1) IS the A and B
 // fragment MMA2 needs once the query index k of MMA2 is relabelled (k = tig <-> query 2tig,
 // k = tig + 4 <-> query 2tig + 1; the sum over queries does not care), so z~ never leaves the
-// registers. Ahat costs 16 registers per lane (hi | lo), S' 8, t' 2. The per-tile Xhat fragments
+// registers. With V = V_h + V_l, S' = sum s V_h V_h^T + M + M^T (M = sum s V_h V_l^T) takes two MMAs
+// per column block where the plain 3xTF32 product u z^T takes three (same products kept, same lo.lo
+// dropped); M^T is formed once per (tile, Gaussian) in shared memory. Ahat costs 16 registers per lane
+// (hi | lo), S' and M 8 each, t' 2. The per-tile Xhat fragments
 // (hi | lo, x - 1/2 as in K5) are built once per work item in shared memory and read as LDS.128.
 //
 // Ahat / bias / colour come from the K5 tensor-core record (rec_tc, ndg_tc_records): row i of Ahat is
@@ -29,14 +32,11 @@ using namespace ndg;
 
 namespace {
 
-#ifndef NDG_MMA_GPW
-#define NDG_MMA_GPW 2
-#endif
 #ifndef NDG_MMA_MINB
 #define NDG_MMA_MINB 4
 #endif
 constexpr int kThreads = 128;   // 4 warps; work item = (tile, chunk of kBwdChunk candidates)
-constexpr int kGpw = NDG_MMA_GPW;   // Gaussians per warp in flight (independent MMA chains)
+constexpr int kGpw = 2;         // Gaussians per warp in flight: the packed dims-8..15 k-step carries two
 
 __device__ __forceinline__ void mma8(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
+    float* sM = reinterpret_cast<float*>(sQ + tile) + warp * 16 * 17;   // per-warp M^T scratch
     const int64_t w = blockIdx.x;
     int64_t lo = 0, hi = T;                   // tile t with chunk_off[t] <= w < chunk_off[t+1]
     while (hi - lo > 1) {
@@ -104,10 +105,15 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
 
     for (int gb = warp * kGpw; gb < n_here; gb += 4 * kGpw) {
         // ---- per-Gaussian operands (warp-uniform Gaussian; an absent second one runs on zeros) ----
-        Split4 ah[kGpw][2];                   // Ahat A-fragments per k-step, hi | lo
+        // Ahat is lower triangular, so its k-step over dims 8..15 has zero rows 0..7: that k-step runs ONE
+        // MMA for both Gaussians in flight, rows 0..7 = Gaussian 0's Ahat[8:16, 8:16], rows 8..15 =
+        // Gaussian 1's (the B operand, the queries, is shared). Its C fragment then holds dims 8+gid of
+        // Gaussian 0 in c0, c1 and of Gaussian 1 in c2, c3 -- the registers each Gaussian's z~ needs.
+        Split4 a0f[kGpw], apk;                // Ahat[:, 0:8] per Gaussian; packed Ahat[8:16, 8:16] pair
         float bz[kGpw][2], col[kGpw][3];
         int64_t e[kGpw];
         bool live[kGpw];
+        float pk[kGpw][2];
 #pragma unroll
         for (int j = 0; j < kGpw; ++j) {
             live[j] = gb + j < n_here;
@@ -116,16 +122,17 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
             auto at = [&](int i, int k) -> float {
                 return (live[j] && i < N && k < N) ? __ldg(r + ((k / 4) * N + i) * 4 + (k & 3)) : 0.f;
             };
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks)
-                ah[j][ks].set(at(gid, ks * 8 + tig), at(gid + 8, ks * 8 + tig), at(gid, ks * 8 + tig + 4),
-                              at(gid + 8, ks * 8 + tig + 4));
+            a0f[j].set(at(gid, tig), at(gid + 8, tig), at(gid, tig + 4), at(gid + 8, tig + 4));
+            pk[j][0] = at(8 + gid, 8 + tig);
+            pk[j][1] = at(8 + gid, 12 + tig);
             bz[j][0] = (live[j] && gid < N) ? __ldg(r + ((N / 4) * N + gid) * 4 + (N & 3)) : 0.f;
             bz[j][1] = (live[j] && gid + 8 < N) ? __ldg(r + ((N / 4) * N + gid + 8) * 4 + (N & 3)) : 0.f;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) col[j][ch] = live[j] ? __ldg(r + N * K + ch) : 0.f;
         }
-        float S[kGpw][2][4] = {}, tz[kGpw][2] = {}, gA[kGpw][3] = {}, ls[kGpw] = {}, px[kGpw] = {};
+        apk.set(pk[0][0], pk[1][0], pk[0][1], pk[1][1]);
+        float S[kGpw][2][4] = {}, Mx[kGpw][2][4] = {};   // sum s v_h v_h^T and sum s v_h v_l^T fragments
+        float tz[kGpw][2] = {}, gA[kGpw][3] = {}, ls[kGpw] = {}, px[kGpw] = {};
 
         for (int nt = 0; nt < tile / 8; ++nt) {
             const float4 xa = sX[nt * 64 + lane], xb = sX[nt * 64 + 32 + lane];
@@ -134,19 +141,23 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                                        {__float_as_uint(xb.x), __float_as_uint(xb.y)}};
             const uint32_t xl[2][2] = {{__float_as_uint(xa.z), __float_as_uint(xa.w)},
                                        {__float_as_uint(xb.z), __float_as_uint(xb.w)}};
+            // MMA1, k-step 1 (dims 8..15) for both Gaussians at once; biases of dims 8+gid in the accumulator
+            float zp[4] = {bz[0][1], bz[0][1], bz[1][1], bz[1][1]}, zpc[4] = {0.f, 0.f, 0.f, 0.f};
+            mma8(zpc, apk.lo, xh[1][0], xh[1][1]);
+            mma8(zpc, apk.hi, xl[1][0], xl[1][1]);
+            mma8(zp, apk.hi, xh[1][0], xh[1][1]);
 #pragma unroll
             for (int j = 0; j < kGpw; ++j) {
-                // MMA1: z~ block, bias in the accumulator, correction products in a second chain
-                float z[4] = {bz[j][0], bz[j][0], bz[j][1], bz[j][1]};
-                float zc[2][4] = {};
-#pragma unroll
-                for (int ks = 0; ks < 2; ++ks) {
-                    mma8(zc[ks], ah[j][ks].lo, xh[ks][0], xh[ks][1]);
-                    mma8(zc[ks], ah[j][ks].hi, xl[ks][0], xl[ks][1]);
-                    mma8(z, ah[j][ks].hi, xh[ks][0], xh[ks][1]);
-                }
-#pragma unroll
-                for (int i = 0; i < 4; ++i) z[i] += zc[0][i] + zc[1][i];
+                // MMA1, k-step 0 (dims 0..7) per Gaussian: bias of dims gid in the accumulator
+                float z[4] = {bz[j][0], bz[j][0], 0.f, 0.f};
+                float zc[4] = {0.f, 0.f, 0.f, 0.f};
+                mma8(zc, a0f[j].lo, xh[0][0], xh[0][1]);
+                mma8(zc, a0f[j].hi, xl[0][0], xl[0][1]);
+                mma8(z, a0f[j].hi, xh[0][0], xh[0][1]);
+                z[0] += zc[0];
+                z[1] += zc[1];
+                z[2] += zc[2] + (zp[2 * j] + zpc[2 * j]);
+                z[3] += zc[3] + (zp[2 * j + 1] + zpc[2 * j + 1]);
                 // s~ of queries 2tig (a) and 2tig+1 (b): this lane's two dims, then over the 8 gid lanes
                 float sa = fmaf(z[2], z[2], z[0] * z[0]), sb = fmaf(z[3], z[3], z[1] * z[1]);
 #pragma unroll
@@ -158,20 +169,22 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                 const float ha = fmaf(qa.z, col[j][2], fmaf(qa.y, col[j][1], qa.x * col[j][0]));
                 const float hb = fmaf(qb.z, col[j][2], fmaf(qb.y, col[j][1], qb.x * col[j][0]));
                 const float wa = ga * ha, wb = gb2 * hb;
-                // MMA2 operands: A = u = w z~ (rows = dims, k = relabelled queries), B = z~
-                const float u0 = wa * z[0], u1 = wa * z[2], u2 = wb * z[1], u3 = wb * z[3];
-                tz[j][0] += u0 + u2;
-                tz[j][1] += u1 + u3;
-                Split4 us, zs;
-                us.set(u0, u1, u2, u3);
-                zs.set(z[0], z[1], z[2], z[3]);
-                // n-tile 0: columns = dims 0..7 (b = z~(gid, q)); n-tile 1: dims 8..15 (b = z~(gid+8, q))
-                mma8(S[j][0], us.lo, zs.hi[0], zs.hi[1]);
-                mma8(S[j][1], us.lo, zs.hi[2], zs.hi[3]);
-                mma8(S[j][0], us.hi, zs.lo[0], zs.lo[1]);
-                mma8(S[j][1], us.hi, zs.lo[2], zs.lo[3]);
-                mma8(S[j][0], us.hi, zs.hi[0], zs.hi[1]);
-                mma8(S[j][1], us.hi, zs.hi[2], zs.hi[3]);
+                tz[j][0] = fmaf(wa, z[0], fmaf(wb, z[1], tz[j][0]));
+                tz[j][1] = fmaf(wa, z[2], fmaf(wb, z[3], tz[j][1]));
+                // S' = sum w z~ z~^T = sum s v v^T with v = sqrt|w| z~, s = sign w. Split v = v_h + v_l:
+                // S' = sum s v_h v_h^T + M + M^T (M = sum s v_h v_l^T; v_l v_l^T dropped as in 3xTF32),
+                // 2 MMAs per column block instead of 3. A = s v_h (rows = dims, k = relabelled queries),
+                // B = v_h | v_l; C-fragment order [c0..c3] = (gid, qa), (gid, qb), (gid+8, qa), (gid+8, qb).
+                const float ra = sqrt_approx(fabsf(wa)), rb = sqrt_approx(fabsf(wb));
+                Split4 vs;
+                vs.set(ra * z[0], rb * z[1], ra * z[2], rb * z[3]);
+                const uint32_t sga = __float_as_uint(wa) & 0x80000000u, sgb = __float_as_uint(wb) & 0x80000000u;
+                const uint32_t av[4] = {vs.hi[0] ^ sga, vs.hi[2] ^ sga, vs.hi[1] ^ sgb, vs.hi[3] ^ sgb};
+                // column block 0 = dims 0..7 (b = v(gid, q)); block 1 = dims 8..15 (b = v(gid+8, q))
+                mma8(Mx[j][0], av, vs.lo[0], vs.lo[1]);
+                mma8(Mx[j][1], av, vs.lo[2], vs.lo[3]);
+                mma8(S[j][0], av, vs.hi[0], vs.hi[1]);
+                mma8(S[j][1], av, vs.hi[2], vs.hi[3]);
                 gA[j][0] = fmaf(ga, qa.x, fmaf(gb2, qb.x, gA[j][0]));
                 gA[j][1] = fmaf(ga, qa.y, fmaf(gb2, qb.y, gA[j][1]));
                 gA[j][2] = fmaf(ga, qa.z, fmaf(gb2, qb.z, gA[j][2]));
@@ -185,13 +198,22 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
         for (int j = 0; j < kGpw; ++j) {
             if (!live[j]) continue;                       // warp-uniform
             double* out = accum + e[j] * A;
+            // S'[r][c] = P[r][c] + M[r][c] + M[c][r]: M^T through this warp's 16 x 17 scratch
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    sM[(gid + (v >> 1) * 8) * 17 + nb * 8 + 2 * tig + (v & 1)] = Mx[j][nb][v];
+            __syncwarp();
 #pragma unroll
             for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
                     const int row = gid + (v >> 1) * 8, colj = nb * 8 + 2 * tig + (v & 1);
-                    if (row < N && colj <= row) atomicAdd(out + tri(row, colj), (double)S[j][nb][v]);
+                    if (row < N && colj <= row)
+                        atomicAdd(out + tri(row, colj), (double)(S[j][nb][v] + Mx[j][nb][v] + sM[colj * 17 + row]));
                 }
+            __syncwarp();
             float r[7] = {tz[j][0], tz[j][1], gA[j][0], gA[j][1], gA[j][2], ls[j], px[j]};
 #pragma unroll
             for (int i = 0; i < 7; ++i) {
@@ -218,7 +240,7 @@ template <int N>
 int launch_backward_mma(int64_t B, int tile, const float* qrec, const float* rec_tc, const int64_t* off,
                         const int32_t* idx, const int64_t* chunk_off, int64_t n_chunks, double* accum, cudaStream_t st) {
     const int64_t T = B / tile;
-    const size_t smem = sizeof(float4) * ((size_t)tile * 8 + tile);
+    const size_t smem = sizeof(float4) * ((size_t)tile * 8 + tile) + sizeof(float) * 4 * 16 * 17;
     static DeviceOnce attr;
     if (attr.first())
         cudaFuncSetAttribute(backward_mma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

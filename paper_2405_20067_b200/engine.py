@@ -9,8 +9,8 @@ gmm-core, culling and grad modules, each enqueued on the current CUDA stream thr
     K4 ndg_cull_*        cull_tile for every tile -> CSR candidate lists
     K5 ndg_forward_tc    eval_mixture (+ K6 loss_rel_l2 fused), tcgen05
        ndg_forward       (FP32-pipe K5: ill-conditioned mixtures, tiles > 256, NDG_FORWARD=fp32)
-    K7 ndg_backward      backward pair loop, FP32 pipe (N <= 15)
-       ndg_backward_mma  (warp-MMA pair loop: N = 16, or NDG_BACKWARD=mma for N >= 9)
+    K7 ndg_backward      backward pair loop, FP32 pipe (N <= 14)
+       ndg_backward_mma  (warp-MMA pair loop: N >= 15, or NDG_BACKWARD=mma for N >= 9)
        ndg_backward_tc   (opt-in NDG_BACKWARD=tc: tcgen05 z-GEMM + moments, N <= 12)
     K7b ndg_moments_to_zspace  x-space moments -> S', t' (tcgen05 K7 only)
     K8 ndg_epilogue      backward tail, raw-parameter chain rule
@@ -297,9 +297,9 @@ class HotPath:
 
     # The warp-MMA K7 forms z~ with the K5 z-GEMM (same records, same error ~2e-7 * RMS(B)), so it
     # shares the tensor-core forward's bound. Its cost does not depend on N (dims pad to one m16
-    # block); the FP32 K7's grows with N and spills from 13 on. Measured crossover (50k Gaussians,
-    # 2^18 queries): 122 vs 272 ms at N=13, 270 vs 269 at 15, 330 vs 266 at 16.
-    MMA_MIN_N = 16
+    # block); the FP32 K7's grows with N and spills from 13 on. Measured (FP32 vs MMA, 50k Gaussians,
+    # 2^18 queries): 122 vs 235 ms at N=13, 186 vs 237 at 14, 271 vs 236 at 15, 330 vs 237 at 16.
+    MMA_MIN_N = 15
 
     def backward_mma_ok(self, recs: EvalRecords) -> bool:
         return (self.backward_impl == "mma" and recs.rec_tc is not None
