@@ -1,7 +1,7 @@
 """Seeded random sweep of the whole hot path against the float64 oracle: dimension, mixture size,
 tile size (including non-powers of two, tiles smaller than one 128-query MMA half and tiles larger
-than the tensor-core forward's 256), children, amplitude mode, query regime and both implementations
-of K5 and K7. Same bars as test_gpu_parity.py (CSR bit-exact, 1e-4 block-relative).
+than the tensor-core forward's 256), children, amplitude mode, query regime and every implementation
+of K5 (tcgen05, FP32) and K7 (FP32, warp-MMA for N >= 9, tcgen05 moments for N <= 12). Same bars as test_gpu_parity.py (CSR bit-exact, 1e-4 block-relative).
 NDG_FUZZ_CASES / NDG_FUZZ_SEED widen the sweep (default 24 cases)."""
 import os
 
@@ -24,7 +24,8 @@ def _cases(n_cases=int(os.environ.get("NDG_FUZZ_CASES", "24")), seed=int(os.envi
         T = int(rng.integers(1, 5))
         G = int(rng.integers(1, 400))
         fwd = str(rng.choice(["tc", "fp32"]))
-        bwd = str(rng.choice(["tc", "fp32"])) if N <= 12 else "fp32"
+        bwds = (["tc"] if N <= 12 else []) + ["fp32"] + (["mma"] if N >= 9 else [])
+        bwd = str(rng.choice(bwds))
         out.append(dict(N=N, tile=tile, B=tile * T, G=G, children=bool(rng.integers(0, 2)),
                         amp_mode=int(rng.integers(0, 2)), regime=str(rng.choice(["R", "C"])), fwd=fwd, bwd=bwd,
                         sigma0=0.3 if bwd == "tc" else None, seed=int(rng.integers(0, 1000))))
