@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
     float4* sQ = smem4 + (tile / 8) * 64;     // [tile] {dpred0, dpred1, dpred2, ell}
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int gid = lane >> 2, tig = lane & 3;
+    const int gid = lane >> 2, tig = lane & 3, odd = gid & 1;
     float* sM = reinterpret_cast<float*>(sQ + tile) + warp * 16 * 17;   // per-warp M^T scratch
     const int64_t w = blockIdx.x;
     int64_t lo = 0, hi = T;                   // tile t with chunk_off[t] <= w < chunk_off[t+1]
@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
 
         for (int nt = 0; nt < tile / 8; ++nt) {
             const float4 xa = sX[nt * 64 + lane], xb = sX[nt * 64 + 32 + lane];
-            const float4 qa = sQ[nt * 8 + 2 * tig], qb = sQ[nt * 8 + 2 * tig + 1];
+            // this lane's own query of the pair (2tig + odd): the per-query scalars are computed once per
+            // lane pair (gid, gid ^ 1) instead of by all eight gid lanes
+            const float4 qm = sQ[nt * 8 + 2 * tig + odd];
             const uint32_t xh[2][2] = {{__float_as_uint(xa.x), __float_as_uint(xa.y)},
                                        {__float_as_uint(xb.x), __float_as_uint(xb.y)}};
             const uint32_t xl[2][2] = {{__float_as_uint(xa.z), __float_as_uint(xa.w)},
@@ -158,24 +160,29 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                 z[1] += zc[1];
                 z[2] += zc[2] + (zp[2 * j] + zpc[2 * j]);
                 z[3] += zc[3] + (zp[2 * j + 1] + zpc[2 * j + 1]);
-                // s~ of queries 2tig (a) and 2tig+1 (b): this lane's two dims, then over the 8 gid lanes
-                float sa = fmaf(z[2], z[2], z[0] * z[0]), sb = fmaf(z[3], z[3], z[1] * z[1]);
-#pragma unroll
-                for (int m = 4; m < 32; m <<= 1) {
-                    sa += __shfl_xor_sync(0xffffffffu, sa, m);
-                    sb += __shfl_xor_sync(0xffffffffu, sb, m);
-                }
-                const float ga = ex2_neg(sa), gb2 = ex2_neg(sb);
-                const float ha = fmaf(qa.z, col[j][2], fmaf(qa.y, col[j][1], qa.x * col[j][0]));
-                const float hb = fmaf(qb.z, col[j][2], fmaf(qb.y, col[j][1], qb.x * col[j][0]));
-                const float wa = ga * ha, wb = gb2 * hb;
+                // s~ of queries 2tig (a) and 2tig+1 (b) from this lane's two dims, reduce-scattered over the
+                // 8 gid lanes: even gid ends with s~(a), odd gid with s~(b)
+                const float sa = fmaf(z[2], z[2], z[0] * z[0]), sb = fmaf(z[3], z[3], z[1] * z[1]);
+                float sm = (odd ? sb : sa) + __shfl_xor_sync(0xffffffffu, odd ? sa : sb, 4);
+                sm += __shfl_xor_sync(0xffffffffu, sm, 8);
+                sm += __shfl_xor_sync(0xffffffffu, sm, 16);
+                const float gm = ex2_neg(sm);
+                const float wm = gm * fmaf(qm.z, col[j][2], fmaf(qm.y, col[j][1], qm.x * col[j][0]));
+                const float rm = sqrt_approx(fabsf(wm));
+                gA[j][0] = fmaf(gm, qm.x, gA[j][0]);
+                gA[j][1] = fmaf(gm, qm.y, gA[j][1]);
+                gA[j][2] = fmaf(gm, qm.z, gA[j][2]);
+                ls[j] = fmaf(gm, qm.w, ls[j]);
+                px[j] = fmaf(fabsf(wm), sqrt_approx(sm), px[j]);
+                const float wo = __shfl_xor_sync(0xffffffffu, wm, 4), ro = __shfl_xor_sync(0xffffffffu, rm, 4);
+                const float wa = odd ? wo : wm, wb = odd ? wm : wo;
+                const float ra = odd ? ro : rm, rb = odd ? rm : ro;
                 tz[j][0] = fmaf(wa, z[0], fmaf(wb, z[1], tz[j][0]));
                 tz[j][1] = fmaf(wa, z[2], fmaf(wb, z[3], tz[j][1]));
                 // S' = sum w z~ z~^T = sum s v v^T with v = sqrt|w| z~, s = sign w. Split v = v_h + v_l:
                 // S' = sum s v_h v_h^T + M + M^T (M = sum s v_h v_l^T; v_l v_l^T dropped as in 3xTF32),
                 // 2 MMAs per column block instead of 3. A = s v_h (rows = dims, k = relabelled queries),
                 // B = v_h | v_l; C-fragment order [c0..c3] = (gid, qa), (gid, qb), (gid+8, qa), (gid+8, qb).
-                const float ra = sqrt_approx(fabsf(wa)), rb = sqrt_approx(fabsf(wb));
                 Split4 vs;
                 vs.set(ra * z[0], rb * z[1], ra * z[2], rb * z[3]);
                 const uint32_t sga = __float_as_uint(wa) & 0x80000000u, sgb = __float_as_uint(wb) & 0x80000000u;
@@ -185,11 +192,6 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                 mma8(Mx[j][1], av, vs.lo[2], vs.lo[3]);
                 mma8(S[j][0], av, vs.hi[0], vs.hi[1]);
                 mma8(S[j][1], av, vs.hi[2], vs.hi[3]);
-                gA[j][0] = fmaf(ga, qa.x, fmaf(gb2, qb.x, gA[j][0]));
-                gA[j][1] = fmaf(ga, qa.y, fmaf(gb2, qb.y, gA[j][1]));
-                gA[j][2] = fmaf(ga, qa.z, fmaf(gb2, qb.z, gA[j][2]));
-                ls[j] = fmaf(ga, qa.w, fmaf(gb2, qb.w, ls[j]));
-                px[j] = fmaf(fabsf(wa), sqrt_approx(sa), fmaf(fabsf(wb), sqrt_approx(sb), px[j]));
             }
         }
 
@@ -220,6 +222,8 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                 r[i] += __shfl_xor_sync(0xffffffffu, r[i], 1);
                 r[i] += __shfl_xor_sync(0xffffffffu, r[i], 2);
             }
+#pragma unroll
+            for (int i = 2; i < 7; ++i) r[i] += __shfl_xor_sync(0xffffffffu, r[i], 4);   // both queries of a pair
             if (tig == 0) {
                 atomicAdd(out + P + gid, (double)r[0]);
                 if (gid + 8 < N) atomicAdd(out + P + gid + 8, (double)r[1]);
