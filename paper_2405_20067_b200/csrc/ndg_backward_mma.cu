@@ -143,23 +143,20 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                                        {__float_as_uint(xb.x), __float_as_uint(xb.y)}};
             const uint32_t xl[2][2] = {{__float_as_uint(xa.z), __float_as_uint(xa.w)},
                                        {__float_as_uint(xb.z), __float_as_uint(xb.w)}};
-            // MMA1, k-step 1 (dims 8..15) for both Gaussians at once; biases of dims 8+gid in the accumulator
-            float zp[4] = {bz[0][1], bz[0][1], bz[1][1], bz[1][1]}, zpc[4] = {0.f, 0.f, 0.f, 0.f};
-            mma8(zpc, apk.lo, xh[1][0], xh[1][1]);
-            mma8(zpc, apk.hi, xl[1][0], xl[1][1]);
+            // MMA1, k-step 1 (dims 8..15) for both Gaussians at once; biases of dims 8+gid in the accumulator,
+            // the two correction products before hi.hi, all in one chain (fewer adds; the loop is issue-bound)
+            float zp[4] = {bz[0][1], bz[0][1], bz[1][1], bz[1][1]};
+            mma8(zp, apk.lo, xh[1][0], xh[1][1]);
+            mma8(zp, apk.hi, xl[1][0], xl[1][1]);
             mma8(zp, apk.hi, xh[1][0], xh[1][1]);
 #pragma unroll
             for (int j = 0; j < kGpw; ++j) {
-                // MMA1, k-step 0 (dims 0..7) per Gaussian: bias of dims gid in the accumulator
-                float z[4] = {bz[j][0], bz[j][0], 0.f, 0.f};
-                float zc[4] = {0.f, 0.f, 0.f, 0.f};
-                mma8(zc, a0f[j].lo, xh[0][0], xh[0][1]);
-                mma8(zc, a0f[j].hi, xl[0][0], xl[0][1]);
+                // MMA1, k-step 0 (dims 0..7) per Gaussian, accumulating onto the bias of dims gid and the
+                // packed k-step's dims 8+gid
+                float z[4] = {bz[j][0], bz[j][0], zp[2 * j], zp[2 * j + 1]};
+                mma8(z, a0f[j].lo, xh[0][0], xh[0][1]);
+                mma8(z, a0f[j].hi, xl[0][0], xl[0][1]);
                 mma8(z, a0f[j].hi, xh[0][0], xh[0][1]);
-                z[0] += zc[0];
-                z[1] += zc[1];
-                z[2] += zc[2] + (zp[2 * j] + zpc[2 * j]);
-                z[3] += zc[3] + (zp[2 * j + 1] + zpc[2 * j + 1]);
                 // s~ of queries 2tig (a) and 2tig+1 (b) from this lane's two dims, reduce-scattered over the
                 // 8 gid lanes: even gid ends with s~(a), odd gid with s~(b)
                 const float sa = fmaf(z[2], z[2], z[0] * z[0]), sb = fmaf(z[3], z[3], z[1] * z[1]);

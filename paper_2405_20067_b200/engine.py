@@ -298,7 +298,7 @@ class HotPath:
     # The warp-MMA K7 forms z~ with the K5 z-GEMM (same records, same error ~2e-7 * RMS(B)), so it
     # shares the tensor-core forward's bound. Its cost does not depend on N (dims pad to one m16
     # block); the FP32 K7's grows with N and spills from 13 on. Measured (FP32 vs MMA, 50k Gaussians,
-    # 2^18 queries): 122 vs ~222 ms at N=13, 187 vs 224 at 14, 272 vs 220 at 15, 330 vs 222 at 16.
+    # 2^18 queries): 122 vs ~208 ms at N=13, 187 vs ~210 at 14, 270 vs 207 at 15, 331 vs 210 at 16.
     MMA_MIN_N = 15
 
     def backward_mma_ok(self, recs: EvalRecords) -> bool:
