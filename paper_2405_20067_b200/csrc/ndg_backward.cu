@@ -24,6 +24,10 @@ __host__ __device__ constexpr int srow_start(int i) {   // sum_{r<i} (r/2 + 1): 
     for (int r = 0; r < i; ++r) s += r / 2 + 1;
     return s;
 }
+#ifndef NDG_BWD_QUNROLL
+#define NDG_BWD_QUNROLL 1   // query-loop unroll factor; tuning builds only
+#endif
+constexpr int kQUnroll = NDG_BWD_QUNROLL;
 #ifndef NDG_BWD_MINB
 #define NDG_BWD_MINB 3   // CTAs per SM the register budget is sized for (N <= 10); tuning builds only
 #endif
@@ -91,6 +95,7 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     for (int i = 0; i < NSP; ++i) Sp[i] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < NZP; ++i) tv2[i] = make_float2(0.f, 0.f);
+#pragma unroll kQUnroll
     for (int q = 0; q < tile; ++q) {
         float xq[QS];
         const float4* q4 = reinterpret_cast<const float4*>(s_q + q * QS);
