@@ -82,6 +82,9 @@ def cpu_sample(a, mix_np, q, t, R, target_s):
     from oracle import ndg_oracle as O
 
     CO.build()
+    # torchrun exports OMP_NUM_THREADS=1 to every rank; the baseline runs on rank 0 alone and uses
+    # every host core it is allowed on
+    CO.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
     threads = CO.max_threads()
     om = O.OMixture(a.n_dims, 0, mix_np["params"].astype(np.float64), mix_np["child"].astype(np.float64),
                     mix_np["has_child"], mix_np["frozen"])
@@ -438,7 +441,7 @@ def our_arm(a, rank, world):
                     global_batch=a.batch * world, tile=a.tile, k=a.k, multiplier=3.0, regime=a.regime,
                     kept_fraction=main["kept"], pairs_per_step=pairs, sigma0=main["sigma0"],
                     l2="flushed before every timed step (256 MiB write, outside the timed interval)",
-                    parallelism=f"dp{world} (tiles sharded, mixture replicated, 1 NCCL allreduce/step)"),
+                    parallelism=f"dp{world} (tiles sharded, mixture replicated, 1 {(dist.get_backend() if dist else 'nccl').upper()} allreduce/step)"),
         roofline=(dict(bound="tensor", kernel=dom, achieved=kern[dom]["tensor_tflops"],
                        peak=kern[dom]["tensor_peak_measured"], unit="TFLOP/s",
                        frac=kern[dom]["frac_of_measured_hmma"], traffic=traffic,
