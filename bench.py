@@ -16,7 +16,8 @@ loss read back. Rank 0 prints one JSON line.
 --impl reference times the reference's CPU path on the host cores: the reference ships no
 runnable implementation, so this is oracle/ndg_oracle.c -- the C/OpenMP
 restatement of SPEC.md standing in for the reference's intended `_core` (pkg/setup.py:36-43) --
-on a bounded sample of the same workload, extrapolated per tile to the full batch.
+on a bounded sample of the same workload (whole tiles x all Gaussians, every stage parallel within a
+tile so all host threads are busy); its rate is the sample's queries over its measured wall time.
 """
 from __future__ import annotations
 
@@ -72,10 +73,22 @@ def workload_name(a, regime):
 # ------------------------------------------------------------------------------------------------
 # CPU baseline (oracle/ndg_oracle.c, all host threads, bounded sample)
 # ------------------------------------------------------------------------------------------------
-def cpu_sample(a, mix_np, q, t, R, target_s):
-    """Time the C/OpenMP restatement on the first S tiles of the workload; return the extrapolated
-    full-batch step time. Fixed per-Gaussian costs (activation, projections, epilogue) are timed
-    once and counted once per step; per-tile costs (bounds, cull, forward, loss, backward) scale."""
+def _sample_tiles(q, t, tile, S):
+    """S whole tiles spread evenly over the batch (tile i*T/S), gathered contiguously."""
+    import numpy as np
+    T = q.shape[0] // tile
+    sel = (np.arange(S) * T) // S
+    rows = (sel[:, None] * tile + np.arange(tile)[None, :]).reshape(-1)
+    return np.ascontiguousarray(q[rows]), np.ascontiguousarray(t[rows])
+
+
+def cpu_sample(a, mix_np, q, t, R, target_s, steps=1, warmup=0):
+    """Time the C/OpenMP restatement (oracle/ndg_oracle.c, every host thread) on a bounded sample of
+    the workload: S whole tiles spread over the batch x ALL Gaussians, one full step each (activation,
+    projections, tile bounds, cull, forward, loss, backward, epilogue). Every stage is parallel WITHIN
+    a tile (queries for the forward, Gaussian blocks for the cull and the backward), so one tile
+    already keeps every thread busy. The reported rate is the sample's own queries / its measured
+    wall time -- no extrapolation -- with the per-Gaussian fixed costs paid once per sampled step."""
     import numpy as np
 
     from oracle import c_oracle as CO
@@ -91,29 +104,34 @@ def cpu_sample(a, mix_np, q, t, R, target_s):
     T = q.shape[0] // a.tile
 
     def run(S):
-        tm = {}
-        n = S * a.tile
-        t0 = time.perf_counter()
-        CO.step(om, q[:n], t[:n], R, tile=a.tile, n_total=q.shape[0], timings=tm)
-        wall = time.perf_counter() - t0
-        fixed = tm["eval_set"] + tm["project"] + tm["epilogue"]
-        return wall, fixed, wall - fixed
+        qs, ts = _sample_tiles(q, t, a.tile, S)
+        t0, c0 = time.perf_counter(), time.process_time()
+        CO.step(om, qs, ts, R, tile=a.tile, n_total=q.shape[0])
+        return time.perf_counter() - t0, time.process_time() - c0
 
-    _, fixed1, var1 = run(1)
-    S = int(max(1, min(T, target_s / max(var1, 1e-6))))
-    wall, fixed, var = run(S)
-    est = fixed + var / S * T
-    return dict(step_s=est, sample_s=wall, tiles=S, threads=threads,
-                sample=f"first {S} of {T} tiles ({S * a.tile} queries) x all {om.G} Gaussians, "
-                       f"per-tile time extrapolated to the full batch + fixed per-Gaussian costs once")
+    w1, _ = run(1)
+    S = int(max(1, min(T, round(target_s / max(w1, 1e-6)))))
+    walls, cpus = [], []
+    for i in range(warmup + steps):
+        w, c = run(S)
+        if i >= warmup:
+            walls.append(w)
+            cpus.append(c)
+    wall = statistics.median(walls)
+    util = sum(cpus) / max(sum(walls), 1e-9) / threads
+    return dict(value=S * a.tile / wall, step_s=wall, walls=walls, tiles=S, threads=threads, utilization=util,
+                queries=S * a.tile,
+                sample=f"{S} of {T} tiles (every {T // S}th, {S * a.tile} queries) x all {om.G} Gaussians per step, "
+                       f"full step (activation .. epilogue) on {threads} threads; value = sampled queries / measured "
+                       f"wall time (no extrapolation); measured CPU utilisation {util:.2f}")
 
 
 def reference_arm(a, rank, world):
-    """--impl reference: the reference's CPU path (C restatement, all host threads), rank 0 only."""
+    """--impl reference: the reference's CPU path (C restatement, all host threads), rank 0 only.
+    A step is one bounded sample of the workload (cpu_sample), sized so W + K steps take a few
+    minutes; ms_per_step is that sample's measured wall time."""
     if rank != 0:
         return
-    import numpy as np
-
     from oracle import ndg_oracle as O
     from paper_2405_20067_b200 import datasets as D
     mix_np, _ = D.synthetic_mixture(a.n_dims, a.gaussians, seed=0, children=a.children)
@@ -121,20 +139,17 @@ def reference_arm(a, rank, world):
     t = D.synthetic_targets(a.batch, seed=3)
     R = O.make_projection_set(a.n_dims, a.k, 2)
     per = max(2.0, min(a.cpu_seconds, 150.0 / max(1, a.steps + a.warmup)))
-    times, info = [], None
-    for i in range(a.warmup + a.steps):
-        info = cpu_sample(a, mix_np, q, t, R, per)
-        if i >= a.warmup:
-            times.append(info["step_s"])
-    step_s = statistics.median(times)
-    v = a.batch / step_s
+    info = cpu_sample(a, mix_np, q, t, R, per, steps=a.steps, warmup=a.warmup)
+    v = info["value"]
     line = dict(metric=METRIC, value=v, unit="queries/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
-                ms_per_step=step_s * 1e3, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
-                data="synthetic", impl="reference",
+                ms_per_step=info["step_s"] * 1e3, higher_is_better=True, scaling="weak", vs_baseline=None,
+                dtype="f64", data="synthetic", impl="reference",
                 config=dict(workload=workload_name(a, a.regime), n_dims=a.n_dims, gaussians=a.gaussians,
-                            batch_per_gpu=a.batch, tile=a.tile, k=a.k, multiplier=3.0, regime=a.regime),
+                            batch_per_gpu=a.batch, tile=a.tile, k=a.k, multiplier=3.0, regime=a.regime,
+                            queries_per_timed_step=info["queries"]),
                 cpu_baseline=dict(value=v, unit="queries/s", cores=info["threads"], kind="port",
-                                  sample=info["sample"], cpu=_cpu_model()),
+                                  sample=info["sample"], cpu=_cpu_model(), utilization=info["utilization"],
+                                  per_step_values=[round(info["queries"] / w, 3) for w in info["walls"]]),
                 e2e=dict(value=v, unit="queries/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
                 note="reference ships no runnable implementation (SURVEY.md §0); timed: oracle/ndg_oracle.c "
                      "(C/OpenMP restatement of SPEC.md, stand-in for the absent compiled _core)")
@@ -472,9 +487,9 @@ def our_arm(a, rank, world):
         line["secondary"] = secondary
     if world == 1 and not a.no_cpu_baseline:
         info = cpu_sample(a, mix_np, q, t, R, a.cpu_seconds)
-        line["cpu_baseline"] = dict(value=a.batch / info["step_s"], unit="queries/s", cores=info["threads"],
+        line["cpu_baseline"] = dict(value=info["value"], unit="queries/s", cores=info["threads"],
                                     kind="port", sample=info["sample"], cpu=_cpu_model(),
-                                    sample_seconds=info["sample_s"])
+                                    sample_seconds=info["step_s"], utilization=info["utilization"])
     print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

@@ -163,26 +163,58 @@ static inline int culled(const double* lo, const double* hi, const double* mr, c
     return 0;
 }
 
-/* cull_tile for every tile, phase 1: counts[T]. */
+/*
+ * cull_tile for every tile. Work items are (tile, block of CULL_EB Gaussians) so
+ * every thread has work even when only a few tiles are culled (a sampled-tile parity check or the
+ * CPU baseline's bounded sample); indices stay ascending because each item writes its own range.
+ */
+#define CULL_EB 2048
+
+static void cull_part_counts(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* mr,
+                             const double* thr, int64_t nb, int64_t* part) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t w = 0; w < T * nb; ++w) {
+        int64_t t = w / nb, e0 = (w % nb) * CULL_EB, e1 = e0 + CULL_EB < Gev ? e0 + CULL_EB : Gev, c = 0;
+        for (int64_t e = e0; e < e1; ++e) c += !culled(lo + t * k, hi + t * k, mr, thr, Gev, k, e);
+        part[w] = c;
+    }
+}
+
+/* phase 1: counts[T]. */
 void ndgo_cull_counts(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* mr,
                       const double* thr, int64_t* counts) {
-#pragma omp parallel for schedule(dynamic, 1)
+    int64_t nb = (Gev + CULL_EB - 1) / CULL_EB;
+    int64_t* part = (int64_t*)calloc((size_t)(T * nb + 1), sizeof(int64_t));
+    cull_part_counts(T, k, Gev, lo, hi, mr, thr, nb, part);
     for (int64_t t = 0; t < T; ++t) {
         int64_t c = 0;
-        for (int64_t e = 0; e < Gev; ++e) c += !culled(lo + t * k, hi + t * k, mr, thr, Gev, k, e);
+        for (int64_t b = 0; b < nb; ++b) c += part[t * nb + b];
         counts[t] = c;
     }
+    free(part);
 }
 
 /* phase 2: ascending candidate indices into idx[offsets[t] .. offsets[t+1]). */
 void ndgo_cull_fill(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* mr,
                     const double* thr, const int64_t* offsets, int32_t* idx) {
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t t = 0; t < T; ++t) {
+    int64_t nb = (Gev + CULL_EB - 1) / CULL_EB;
+    int64_t* part = (int64_t*)calloc((size_t)(T * nb + 1), sizeof(int64_t));
+    cull_part_counts(T, k, Gev, lo, hi, mr, thr, nb, part);
+    for (int64_t t = 0; t < T; ++t) {           /* exclusive prefix within the tile */
         int64_t o = offsets[t];
-        for (int64_t e = 0; e < Gev; ++e)
+        for (int64_t b = 0; b < nb; ++b) {
+            int64_t c = part[t * nb + b];
+            part[t * nb + b] = o;
+            o += c;
+        }
+    }
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t w = 0; w < T * nb; ++w) {
+        int64_t t = w / nb, e0 = (w % nb) * CULL_EB, e1 = e0 + CULL_EB < Gev ? e0 + CULL_EB : Gev, o = part[w];
+        for (int64_t e = e0; e < e1; ++e)
             if (!culled(lo + t * k, hi + t * k, mr, thr, Gev, k, e)) idx[o++] = (int32_t)e;
     }
+    free(part);
 }
 
 static inline double pair_eval(int N, const double* x, const double* m, const double* Le, double* z) {
@@ -196,28 +228,26 @@ static inline double pair_eval(int N, const double* x, const double* m, const do
     return s;
 }
 
-/* eval_mixture over each tile's candidates. pred [B*3]. */
+/* eval_mixture over each tile's candidates. pred [B*3]. Queries are independent
+ * (SPEC.md:136), so the work items are single queries: all threads are busy even on one tile. */
 void ndgo_forward(int N, int64_t B, int tile, const float* q, const double* mean, const double* L,
                   const double* a, const int64_t* offsets, const int32_t* idx, double* pred) {
-    int64_t T = B / tile;
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t t = 0; t < T; ++t) {
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t b = 0; b < B; ++b) {
         double x[NMAX], z[NMAX];
-        for (int qi = 0; qi < tile; ++qi) {
-            int64_t b = t * tile + qi;
-            for (int j = 0; j < N; ++j) x[j] = (double)q[b * N + j];
-            double p0 = 0, p1 = 0, p2 = 0;
-            for (int64_t c = offsets[t]; c < offsets[t + 1]; ++c) {
-                int64_t e = idx[c];
-                double g = exp(-0.5 * pair_eval(N, x, mean + e * N, L + e * N * N, z));
-                p0 += g * a[e * 3];
-                p1 += g * a[e * 3 + 1];
-                p2 += g * a[e * 3 + 2];
-            }
-            pred[b * 3] = p0;
-            pred[b * 3 + 1] = p1;
-            pred[b * 3 + 2] = p2;
+        int64_t t = b / tile;
+        for (int j = 0; j < N; ++j) x[j] = (double)q[b * N + j];
+        double p0 = 0, p1 = 0, p2 = 0;
+        for (int64_t c = offsets[t]; c < offsets[t + 1]; ++c) {
+            int64_t e = idx[c];
+            double g = exp(-0.5 * pair_eval(N, x, mean + e * N, L + e * N * N, z));
+            p0 += g * a[e * 3];
+            p1 += g * a[e * 3 + 1];
+            p2 += g * a[e * 3 + 2];
         }
+        pred[b * 3] = p0;
+        pred[b * 3 + 1] = p1;
+        pred[b * 3 + 2] = p2;
     }
 }
 

@@ -1,0 +1,131 @@
+"""GPU parity at the BENCHMARKED configurations (BASELINE.json configs[1], [3], [4]) at full G.
+
+Every case builds the bench's own inputs (paper_2405_20067_b200.datasets generators, the seeds bench.py
+uses: mixture 0, queries 1, targets 3, projections 2), keeps ALL Gaussians (100k / 500k / 1M, plus
+live children where marked), and takes a sample of whole tiles spread evenly over the benchmark
+batch (tile i*T/S), so the device runs the production kernels on the production mixture while the
+C oracle (oracle/ndg_oracle.c, float64) finishes in seconds. Bars (SPEC.md:198-206, :263-271,
+north_star): candidate lists bit-exact; pred, loss, each raw-gradient block (parent / child) and
+each density statistic within 1e-4 block-relative. The per-element error distribution (max |d| /
+max |ref| per block, and the largest per-coordinate relative error above a 1e-6 * max|ref| floor)
+is printed and, when NDG_PARITY_LOG is set, appended to that file as JSON lines.
+"""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import c_oracle as CO
+from oracle import ndg_oracle as O
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-4
+
+# (label, N, G, B of the benchmark batch, regime, sampled tiles, children, amp_mode, frozen fraction)
+CASES = [
+    ("cfg2-R", 10, 100_000, 1 << 20, "R", 8, False, 0, 0.0),
+    ("cfg2-C", 10, 100_000, 1 << 20, "C", 16, False, 0, 0.0),
+    ("cfg2-R-children", 10, 100_000, 1 << 20, "R", 4, True, 0, 0.0),
+    ("cfg2-C-children-opacity", 10, 100_000, 1 << 20, "C", 8, True, 1, 0.0),
+    ("cfg2-R-children-frozen", 10, 100_000, 1 << 20, "R", 4, True, 0, 0.1),
+    ("cfg4-R", 16, 500_000, 1 << 22, "R", 1, False, 0, 0.0),
+    ("cfg4-C", 16, 500_000, 1 << 22, "C", 2, False, 0, 0.0),
+    ("cfg5-R", 10, 1_000_000, 1 << 19, "R", 1, False, 0, 0.0),
+    ("cfg5-C-children", 10, 1_000_000, 1 << 19, "C", 8, True, 0, 0.0),
+]
+
+_cache = {}
+
+
+def _inputs(N, G, B, regime, children, amp_mode):
+    from paper_2405_20067_b200 import datasets as D
+    # the generator draws the child rows after the parent rows, so one draw with children serves both
+    # variants (children=False just leaves has_child clear)
+    key = ("mix", N, G, amp_mode)
+    if key not in _cache:
+        _cache.clear()                      # keep one configuration's arrays resident at a time
+        _cache[key] = D.synthetic_mixture(N, G, seed=0, children=True, amp_mode=amp_mode)[0]
+    qkey = ("q", N, B, regime)
+    if qkey not in _cache:
+        _cache[qkey] = (D.synthetic_queries(N, B, seed=1, regime=regime), D.synthetic_targets(B, seed=3))
+    rows = dict(_cache[key])
+    if not children:
+        rows["has_child"] = np.zeros_like(rows["has_child"])
+    return rows, _cache[qkey]
+
+
+def _sample(q, t, S, tile=256):
+    T = q.shape[0] // tile
+    sel = (np.arange(S) * T) // S
+    rows = (sel[:, None] * tile + np.arange(tile)[None, :]).reshape(-1)
+    return np.ascontiguousarray(q[rows]), np.ascontiguousarray(t[rows])
+
+
+def _err(got, ref):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    nr = np.linalg.norm(ref)
+    d = np.abs(got - ref)
+    mx = float(np.abs(ref).max()) if ref.size else 0.0
+    floor = 1e-6 * mx
+    big = np.abs(ref) > floor
+    per = float((d[big] / np.abs(ref[big])).max()) if np.any(big) else 0.0
+    return dict(block_rel=float(np.linalg.norm(got - ref) / nr) if nr > 0 else float(np.linalg.norm(got)),
+                max_abs_over_max_ref=float(d.max() / mx) if mx > 0 else float(d.max() if d.size else 0.0),
+                max_elem_rel_floor=per)
+
+
+@pytest.mark.parametrize("label,N,G,B,regime,S,children,amp_mode,frozen_frac", CASES, ids=[c[0] for c in CASES])
+def test_benchmarked_config_parity(cuda, label, N, G, B, regime, S, children, amp_mode, frozen_frac):
+    import paper_2405_20067_b200 as ndg
+    rows, (q_full, t_full) = _inputs(N, G, B, regime, children, amp_mode)
+    frozen = np.zeros(G, bool)
+    if frozen_frac > 0:
+        frozen[np.random.default_rng(11).random(G) < frozen_frac] = True
+    q, t = _sample(q_full, t_full, S)
+    mix = ndg.Mixture.from_arrays(N, amp_mode, rows["params"], rows["child"], rows["has_child"], frozen)
+    hp = ndg.HotPath(N, projection_seed=2)
+    t0 = time.perf_counter()
+    res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    torch.cuda.synchronize()
+    t_gpu = time.perf_counter() - t0
+    om = O.OMixture(N, amp_mode, rows["params"].astype(np.float64), rows["child"].astype(np.float64),
+                    rows["has_child"], frozen)
+    t0 = time.perf_counter()
+    ref = CO.step(om, q, t, hp.ps.vectors)
+    t_cpu = time.perf_counter() - t0
+
+    off, idx = res.candidates.offsets.cpu().numpy(), res.candidates.idx.cpu().numpy()
+    assert np.array_equal(off, ref["offsets"]), f"{label}: CSR offsets differ"
+    assert np.array_equal(idx, ref["idx"]), f"{label}: CSR indices differ"
+    report = dict(case=label, N=N, G=G, Gev=int(res.grads.stats.shape[0]), tiles=S, regime=regime,
+                  children=children, amp_mode=amp_mode, frozen=int(frozen.sum()), nnz=int(off[-1]),
+                  forward=hp.last_forward_impl, backward=hp.last_backward_impl, gpu_s=round(t_gpu, 3),
+                  oracle_s=round(t_cpu, 3), blocks={})
+    report["blocks"]["pred"] = _err(res.pred.cpu().numpy(), ref["pred"])
+    report["blocks"]["loss"] = dict(rel=abs(res.loss - ref["loss"]) / abs(ref["loss"]))
+    ms, cs, cols, amp = O.raw_slices(N)
+    sl = (("mean", ms), ("chol", cs), ("color", cols), ("amp", slice(amp, amp + 1)))
+    which = [("parent", res.grads.params.cpu().numpy(), ref["grad_parent"])]
+    if children:
+        which.append(("child", res.grads.child.cpu().numpy(), ref["grad_child"]))
+    for tag, got, want in which:
+        for name, s in sl:
+            report["blocks"][f"{tag}.{name}"] = _err(got[:, s], want[:, s])
+    st = res.grads.stats.cpu().numpy()
+    for j, name in enumerate(("loss_share", "grad_proxy", "pairs")):
+        report["blocks"][f"stat.{name}"] = _err(st[:, j], ref["stats"][:, j])
+    line = json.dumps(report)
+    print(line)
+    if os.environ.get("NDG_PARITY_LOG"):
+        with open(os.environ["NDG_PARITY_LOG"], "a") as f:
+            f.write(line + "\n")
+    assert report["blocks"]["loss"]["rel"] <= RTOL, label
+    for name, e in report["blocks"].items():
+        if "block_rel" in e:
+            assert e["block_rel"] < RTOL, f"{label}.{name}: block-relative error {e['block_rel']:.3e}"
+    if frozen_frac > 0:
+        gp = res.grads.params.cpu().numpy()
+        assert np.all(gp[frozen] == 0.0), "frozen components must receive no gradient (SPEC.md:388)"
