@@ -292,9 +292,15 @@ def hmma_peak(torch, K, dev):
 def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmup, measure_e2e):
     import numpy as np
 
+    from paper_2405_20067_b200 import parallel as P
     mix_np, s0 = D.synthetic_mixture(a.n_dims, a.gaussians, seed=0, children=a.children)
-    q = D.synthetic_queries(a.n_dims, a.batch, seed=1 + rank, regime=regime, tile_size=a.tile)
-    t = D.synthetic_targets(a.batch, seed=3 + rank)
+    # one global batch of a.batch * world queries; rank r keeps global tiles r, r + world, ... (weak
+    # scaling: a.batch queries per GPU)
+    q = D.synthetic_queries(a.n_dims, a.batch * world, seed=1, regime=regime, tile_size=a.tile)
+    t = D.synthetic_targets(a.batch * world, seed=3)
+    if world > 1:
+        q, t, _ = P.shard_queries(q, t, a.tile, rank, world)
+        q, t = np.ascontiguousarray(q), np.ascontiguousarray(t)
     mix = ndg.Mixture.from_arrays(a.n_dims, ndg.BRIGHTNESS, **mix_np, device=dev)
     hp = ndg.HotPath(a.n_dims, k=a.k, multiplier=3.0, tile_size=a.tile, projection_seed=2, device=dev)
     qd = torch.from_numpy(q).to(dev)
@@ -303,7 +309,7 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
     state = ndg.new_adam_state(mix)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     n_total = a.batch * world
-    allreduce = (lambda flat: dist.all_reduce(flat)) if world > 1 else None
+    allreduce = P.make_allreduce() if world > 1 else None
     it = [0]
 
     def step(queries, targets):
@@ -456,7 +462,9 @@ def our_arm(a, rank, world):
                     global_batch=a.batch * world, tile=a.tile, k=a.k, multiplier=3.0, regime=a.regime,
                     kept_fraction=main["kept"], pairs_per_step=pairs, sigma0=main["sigma0"],
                     l2="flushed before every timed step (256 MiB write, outside the timed interval)",
-                    parallelism=f"dp{world} (tiles sharded, mixture replicated, 1 {(dist.get_backend() if dist else 'nccl').upper()} allreduce/step)"),
+                    parallelism=f"dp{world} (one global batch of {a.batch * world} queries, strided tiles per "
+                                f"rank, mixture replicated, 1 {(dist.get_backend() if dist else 'nccl').upper()} "
+                                f"allreduce/step of the flat gradient buffer)"),
         roofline=(dict(bound="tensor", kernel=dom, achieved=kern[dom]["tensor_tflops"],
                        peak=kern[dom]["tensor_peak_measured"], unit="TFLOP/s",
                        frac=kern[dom]["frac_of_measured_hmma"], traffic=traffic,

@@ -70,7 +70,7 @@ int ndg_supported_dims(int n);
 int ndg_raw_floats(int n);        /* N + P + 4                                       */
 int ndg_record_floats(int n);     /* evaluation record stride (float32, 16-B multiple) */
 int ndg_query_floats(int n);      /* backward query record stride: x[N] | dpred[3] | ell */
-int ndg_accum_doubles(int n);     /* accumulator stride: S[P] | t[N] | gA[3] | stats[3] */
+int ndg_accum_doubles(int n);     /* accumulator stride: S[P] | t[N] | flag | gA[3] | stats[3] */
 int ndg_num_stats(void);          /* density-control statistics per evaluated Gaussian (3) */
 int ndg_backward_chunk(void);     /* candidates per backward work item (chunk_offsets unit) */
 
@@ -138,29 +138,39 @@ int ndg_forward_tc(int n, int64_t B, int tile, const float* queries, const float
                    const float* rec_tc, const int64_t* offsets, const int32_t* idx, float eps, int64_t n_total,
                    float* pred, float* qrec, double* loss_partial, void* stream);
 
+/* Standalone loss_rel_l2 for the module-level API (the step fuses it into K5):
+ * loss_partial[ceil(B/256)] float64 block partials of mean((p - t)^2 / (p^2 + eps)) over 3 * n_total
+ * entries, and dpred[B][3] (may be NULL) with the denominator detached; sum the partials
+ * with ndg_loss_finalize. */
+int ndg_loss_rel_l2(int64_t B, const float* pred, const float* target, float eps, int64_t n_total, float* dpred,
+                    double* loss_partial, void* stream);
+
 /* Deterministic fixed-order sum of the per-tile loss partials. */
 int ndg_loss_finalize(int64_t T, const double* loss_partial, double* loss, void* stream);
+
+/* K7 work items in band order: items[n_chunks] int64 = (tile << 32) | chunk, the band of 512 tiles
+ * chunk-major over the chunks every tile of it has (the CTAs in flight share one candidate chunk's
+ * records and accumulators in L2), tile-major over the rest. A bijection onto the work items that
+ * chunk_offsets (ndg_scan_counts) numbers tile-major. */
+int ndg_work_items(int64_t T, const int64_t* chunk_offsets, int64_t* items, void* stream);
+
+/* Bounds of the deterministic backward reduction: bounds[4] (uint32, zeroed by the caller) receive the
+ * float bit patterns of H = max_q sum_c |dpred_c|, max_q,c |dpred_c|, max_q ell (over qrec[B]) and
+ * max |a_c| over live Gaussians (rec, eflags). Run after the forward, before K7. */
+int ndg_bwd_bounds(int n, int64_t B, const float* qrec, int64_t Gev, const float* rec, const uint8_t* eflags,
+                   uint32_t* bounds, void* stream);
 
 /*
  * K7 fused backward. Replaces the pair loop of `backward`: per (tile, chunk of
  * candidates) one thread per Gaussian sweeps the tile's queries and accumulates the sufficient
- * statistics S, t, gA and the density-control statistics, then adds them to accum[Gev][A]
- * (float64, zeroed by the caller).
+ * statistics S, t, gA and the density-control statistics, then adds them to accum[2][Gev][A] (int64
+ * fixed point: hi words then lo words, zeroed by the caller) with scales derived from `bounds`. The
+ * sums are exact integers, so the result is independent of the order work items run in (SPEC.md:294,
+ * bit-reproducible training :380, :581). `items` from ndg_work_items.
  */
 int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec, int centred, const int64_t* offsets,
-                 const int32_t* idx, const int64_t* chunk_offsets, int64_t n_chunks, double* accum, void* stream);
-
-/*
- * K7 on the tensor cores (tcgen05 kind::tf32, 3xTF32). Same pair loop and the same accum contract as
- * ndg_backward after ndg_moments_to_zspace: one CTA per 128 queries of a tile, z~ by the K5 z-GEMM
- * over rec_tc, then the x-space moments M = sum w xhat xhat^T (xhat = [x - 1/2; 1]) by a second
- * tcgen05 GEMM, added to accum[e][0 .. (N+1)(N+2)/2) (packed lower triangle = quad | lin | const);
- * gA, loss share, proxy and pairs go to the tail as for ndg_backward.
- * Returns NDG_ERR_UNSUPPORTED_DIMS when ndg_backward_tc_supported(n) is 0.
- */
-int ndg_backward_tc_supported(int n);
-int ndg_backward_tc(int n, int64_t B, int tile, const float* qrec, const float* rec_tc, const int64_t* offsets,
-                    const int32_t* idx, double* accum, void* stream);
+                 const int32_t* idx, const int64_t* items, int64_t n_chunks, int64_t Gev, const uint32_t* bounds,
+                 int64_t* accum, void* stream);
 
 /*
  * K7 on warp-level tensor cores for large N (mma.sync m16n8k8 tf32, 3xTF32). Same work items
@@ -172,12 +182,13 @@ int ndg_backward_tc(int n, int64_t B, int tile, const float* qrec, const float* 
  */
 int ndg_backward_mma_supported(int n);
 int ndg_backward_mma(int n, int64_t B, int tile, const float* qrec, const float* rec_tc, const int64_t* offsets,
-                     const int32_t* idx, const int64_t* chunk_offsets, int64_t n_chunks, double* accum, void* stream);
+                     const int32_t* idx, const int64_t* items, int64_t n_chunks, int64_t Gev, const uint32_t* bounds,
+                     int64_t* accum, void* stream);
 
-/* K7b: per live evaluated Gaussian, turn the moments left by ndg_backward_tc into S' = Ahat M Ahat^T
- * and t' = Ahat M[:, N] in place (float64; Ahat = C [L^-1 | L^-1 (1/2 - m)] from K1's factor). */
-int ndg_moments_to_zspace(int n, int64_t Gev, const double* mean64, const double* chol64, const uint8_t* eflags,
-                          double* accum, void* stream);
+/* Fixed point -> float64: accum[2][Gev][A] int64 from K7 becomes float64 accum[Gev][A] in place over its
+ * first half (hi / s + lo / (s 2^40) with the scales of `bounds` and B); a Gaussian whose flag slot is
+ * set (a non-finite or out-of-bound partial) gets NaN in every slot, which K8 reports. */
+int ndg_acc_dequant(int n, int64_t Gev, int64_t B, const uint32_t* bounds, int64_t* accum, void* stream);
 
 /*
  * Diagnostic (not on the training path): brute_force_active for every tile as a
@@ -200,6 +211,17 @@ int ndg_active_mask(int n, int64_t B, int tile, const float* queries, const doub
 int ndg_loss_f64(int n, int G, int amp_mode, int M, const double* params, const double* child, const uint8_t* flags,
                  int64_t B, const float* queries, const float* targets, const double* inv_den, double* pred_out,
                  double* loss, void* stream);
+
+/*
+ * Diagnostic for cmd_gradcheck: the backward pair loop in float64 (culling off, every query, one thread
+ * per evaluated Gaussian) with K7's accumulator contract, written to accum[Gev][A] (float64) for
+ * ndg_epilogue. dpred [B][3] and ell [B] (may be NULL) in float64; a = alpha * sigmoid(color) is
+ * activated in float64 from the raw rows. Lets gradcheck hold the analytic gradient to SPEC.md:572's
+ * per-coordinate bar (the float32 product kernels are checked against the oracle instead).
+ */
+int ndg_backward_f64(int n, int64_t G, int64_t Gev, int amp_mode, const float* params, const float* child,
+                     const double* mean64, const double* chol64, const uint8_t* eflags, int64_t B,
+                     const float* queries, const double* dpred, const double* ell, double* accum, void* stream);
 
 /*
  * K8 epilogue. Replaces the tail of `backward`: raw-parameter gradients of parents

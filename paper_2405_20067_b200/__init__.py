@@ -9,6 +9,11 @@ operations, types and exceptions, with every stage executed by hand-written CUDA
     >>> mix = ndg.Mixture.from_arrays(10, ndg.BRIGHTNESS, params)
     >>> hp = ndg.HotPath(10, k=16, multiplier=3.0, tile_size=256)
     >>> res = hp.fwd_bwd(mix, queries, targets)        # culled forward + rel-L2 loss + backward
+
+The reference's module-level operations are exported under their SPEC names (api.py):
+activate_cholesky, eval_gaussian, eval_mixture, compose_child, make_projection_set,
+project_components, tile_bounds, cull_tile, brute_force_active, loss_rel_l2, backward,
+finite_diff_grad, adam_step.
 """
 from .errors import (ConfigError, DegenerateSliceError, FileFormatError, InvalidParameterError,  # noqa: F401
                      NdgError, NonFiniteGradientError, TrainingAborted)
@@ -17,21 +22,8 @@ from .engine import (CandidateLists, EvalRecords, GradientBuffer, HotPath, Proje
                      ProjectionSet, StepResult, TileBounds, adam_step, alloc_gradients, kept_pairs_flops,
                      make_projection_set, new_adam_state)
 
-__version__ = "0.1.0"
+from .api import (activate_cholesky, backward, brute_force_active, candidate_lists, compose_child,  # noqa: F401
+                  cull_tile, eval_gaussian, eval_mixture, finite_diff_grad, loss_rel_l2, project_components,
+                  tile_bounds)
 
-
-def eval_mixture(mix: Mixture, queries, *, tile_size: int = 256, k: int = 16, multiplier: float = 3.0,
-                 projection_seed: int = 0, cull: bool = True):
-    """Batched, culled eval_mixture at every query; returns pred [B, 3] on device."""
-    hp = HotPath(mix.n_dims, k=k, multiplier=multiplier, tile_size=tile_size, projection_seed=projection_seed,
-                 device=mix.device)
-    return hp.evaluate(mix, queries, cull=cull)
-
-
-def backward(mix: Mixture, queries, targets, *, eps: float = 0.01, tile_size: int = 256, k: int = 16,
-             multiplier: float = 3.0, projection_seed: int = 0, cull: bool = True):
-    """(loss, GradientBuffer) of the relative-L2 loss w.r.t. every raw parameter."""
-    hp = HotPath(mix.n_dims, k=k, multiplier=multiplier, tile_size=tile_size, eps=eps,
-                 projection_seed=projection_seed, device=mix.device)
-    res = hp.fwd_bwd(mix, queries, targets, cull=cull)
-    return res.loss, res.grads
+__version__ = "0.2.0"

@@ -19,7 +19,9 @@ Cauchy-Schwarz; multiplier 1 rows show the paper's artifact regime. (The culled 
 by up to exp(-m^2/2) * sum |a| of the dropped Gaussians, so max_abs_err is reported, not bounded by
 1e-6: DESIGN.md §5.)
 gradcheck compares the analytic gradients with central finite differences of a
-float64 evaluator (paper_2405_20067_b200/gradcheck.py); exit 0 iff the max relative error < 1e-4.
+float64 evaluator (paper_2405_20067_b200/gradcheck.py); exit 0 iff every coordinate's relative error
+(1e-6 absolute floor) is < 1e-4. --fp32 checks the float32 product kernels instead,
+under the relaxed block-relative 1e-4 rule, and says so in its output.
 """
 from __future__ import annotations
 
@@ -50,14 +52,37 @@ def _state_of(tr, cfg_raw):
     m = tr.mix
     return dict(n_dims=m.n_dims, amp_mode=m.amp_mode, iteration=tr.step_no, adam_step=tr.step_no,
                 config=cfg_raw, dataset=cfg_raw.get("data", {}),
-                rng=dict(seed=tr.cfg.seed, numpy=str(tr.rng.bit_generator.state["state"]["state"])),
+                rng=tr.rng_state(),
                 params=m.params.cpu().numpy(), child=m.child.cpu().numpy(), flags=m.flags.cpu().numpy(),
                 m1p=tr.state["m1p"].cpu().numpy(), m2p=tr.state["m2p"].cpu().numpy(),
                 m1c=tr.state["m1c"].cpu().numpy(), m2c=tr.state["m2c"].cpu().numpy(),
                 low_count=tr.low_count.cpu().numpy())
 
 
+def _dist_setup():
+    """torchrun: one process per GPU (RANK / LOCAL_RANK / WORLD_SIZE from the environment), NCCL
+    process group (NDG_DIST_BACKEND=gloo for plumbing checks); returns (rank, world, allreduce)."""
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world <= 1:
+        return 0, 1, None
+    import torch.distributed as dist
+
+    from .parallel import make_allreduce
+    local = int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group(os.environ.get("NDG_DIST_BACKEND", "nccl"))
+    return dist.get_rank(), world, make_allreduce()
+
+
 def cmd_fit(args) -> int:
+    """SPEC.md:511-519. Under torchrun every rank runs this: the mixture and optimizer state are
+    replicated, each rank evaluates its strided tiles of the one global batch (datasets.sample_batch)
+    and the step's gradients are summed by ONE allreduce; rank 0 writes
+    metrics.csv and the checkpoints. --resume continues bit-identically: the checkpoint
+    carries the torch sampling-generator state and the full numpy PCG64 state, and metrics.csv is
+    appended to."""
     import torch
     from .gmm import FLAG_CHILD, FLAG_FROZEN, Mixture
     from .trainer import Trainer
@@ -67,8 +92,14 @@ def cmd_fit(args) -> int:
     except ConfigError as e:
         print(f"config error: {e}", file=sys.stderr)
         return 2
+    rank, world, allreduce = _dist_setup()
+    if cfg.batch_size % cfg.tile_size or cfg.batch_size // cfg.tile_size < world:
+        print(f"config error: batch_size must be a multiple of tile_size with at least one tile per rank "
+              f"({world} ranks)", file=sys.stderr)
+        return 2
     n = int(cfg_raw.get("data", {}).get("n_dims", 10))
-    os.makedirs(args.out, exist_ok=True)
+    if rank == 0:
+        os.makedirs(args.out, exist_ok=True)
     dev = torch.device("cuda", torch.cuda.current_device())
     target = _target(cfg_raw, n, dev)
     mix = None
@@ -78,32 +109,54 @@ def cmd_fit(args) -> int:
         fl = st["flags"]
         mix = Mixture.from_arrays(st["n_dims"], st["amp_mode"], st["params"], st["child"], (fl & FLAG_CHILD) != 0,
                                   (fl & FLAG_FROZEN) != 0, device=dev)
-    tr = Trainer(cfg, target, n, mixture=mix, device=dev)
+    tr = Trainer(cfg, target, n, mixture=mix, device=dev, allreduce=allreduce, rank=rank, world=world)
     if st is not None:
         tr.step_no = int(st["iteration"])
         for k in ("m1p", "m2p", "m1c", "m2c"):
             tr.state[k] = torch.from_numpy(st[k]).to(dev)
         tr.low_count = torch.from_numpy(st["low_count"]).to(dev)
-    metrics = open(os.path.join(args.out, "metrics.csv"), "w")
-    metrics.write("iteration,loss,n_components,culled_fraction,ms_per_iter\n")
+        tr.set_rng_state(st.get("rng", {}))
+    metrics = None
+    if rank == 0:
+        path = os.path.join(args.out, "metrics.csv")
+        fresh = st is None or not os.path.exists(path)
+        metrics = open(path, "w" if fresh else "a")
+        if fresh:
+            metrics.write("iteration,loss,n_components,culled_fraction,ms_per_iter\n")
     ckpt = os.path.join(args.out, "checkpoint.ndgc")
+
+    def save():
+        if rank == 0:
+            nio.save_checkpoint(ckpt, _state_of(tr, cfg_raw))
+
     try:
         start = tr.step_no
         for it in range(start, cfg.iterations):
             row = tr.iteration()
-            metrics.write(f"{row.iteration},{row.loss:.9g},{row.n_components},{row.culled_fraction:.6f},"
-                          f"{row.ms_per_iter:.3f}\n")
+            if metrics:
+                metrics.write(f"{row.iteration},{row.loss:.9g},{row.n_components},{row.culled_fraction:.6f},"
+                              f"{row.ms_per_iter:.3f}\n")
+            if it == start and world > 1 and rank == 0:
+                print(f"data-parallel fit: {world} ranks, allreduce payload {tr.last_allreduce_bytes} bytes/step",
+                      file=sys.stderr)
             if (it + 1) % cfg.phase_length == 0:
                 if (it + 1) // cfg.phase_length >= cfg.warmup_phases:
                     tr.phase_event()
-                nio.save_checkpoint(ckpt, _state_of(tr, cfg_raw))
+                    if world > 1 and rank == 0:
+                        print(f"phase event at {it + 1}: {tr.mix.G} components, children live "
+                              f"{tr.mix.children_live}", file=sys.stderr)
+                save()
     except TrainingAborted as e:
-        nio.save_checkpoint(ckpt, _state_of(tr, cfg_raw))
+        save()
         print(f"training aborted: {e}", file=sys.stderr)
         return 3
     finally:
-        metrics.close()
-    nio.save_checkpoint(ckpt, _state_of(tr, cfg_raw))
+        if metrics:
+            metrics.close()
+    save()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
     return 0
 
 
@@ -246,7 +299,7 @@ def cmd_bench_cull(args) -> int:
 
 def cmd_gradcheck(args) -> int:
     from . import gradcheck
-    return 0 if gradcheck.run(seed=args.seed, per_n=args.per_n) else 1
+    return 0 if gradcheck.run(seed=args.seed, per_n=args.per_n, analytic="fp32" if args.fp32 else "f64") else 1
 
 
 def main(argv=None) -> int:
@@ -270,6 +323,9 @@ def main(argv=None) -> int:
     gc = sub.add_parser("gradcheck")
     gc.add_argument("--seed", type=int, default=0)
     gc.add_argument("--per-n", type=int, default=100, help="random mixtures per (N, amplitude mode)")
+    gc.add_argument("--fp32", action="store_true",
+                    help="check the float32 product kernels under the relaxed block-relative rule instead of "
+                         "SPEC.md:572's per-coordinate rule on the float64 analytic path")
     args = ap.parse_args(argv)
     try:
         return {"fit": cmd_fit, "eval": cmd_eval, "bench-cull": cmd_bench_cull,

@@ -9,8 +9,11 @@
 //   S' += (w z~) z~^T (lower),  t' += w z~,  gA += g dpred
 //   loss_share += g * ell,      proxy += |w| sqrt(s~)        (density-control statistics)
 // so the per-query reduction the query-stationary mapping would need (A(N) warp shuffles per pair)
-// disappears; the only reduction is one float64 atomicAdd per accumulator per (tile, candidate),
-// amortised over the tile's queries. The epilogue (ndg_prep.cu) applies the -1/C^2, -1/C scalings.
+// disappears; the only reduction is one deterministic fixed-point add (two int64 words, ndg_common.cuh)
+// per accumulator per (tile, candidate), amortised over the tile's queries, so the result does not
+// depend on the order work items finish. Work items come in band order (ndg_work_items): the CTAs in
+// flight share their candidates' records and accumulators in L2. ndg_acc_dequant and the epilogue
+// (ndg_prep.cu) turn the words into float64 and apply the -1/C^2, -1/C scalings.
 #include "ndg_common.cuh"
 
 using namespace ndg;
@@ -36,7 +39,8 @@ template <int N, bool CTR>
 __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     backward_kernel(int64_t T, int tile, const float* __restrict__ qrec, const float* __restrict__ rec,
                     const int64_t* __restrict__ offsets, const int32_t* __restrict__ idx,
-                    const int64_t* __restrict__ chunk_off, double* __restrict__ accum) {
+                    const int64_t* __restrict__ items, int64_t Gev, const uint32_t* __restrict__ bounds,
+                    unsigned long long* __restrict__ accum) {
     constexpr int RS = rec_floats(N);
     constexpr int QS = qrec_floats(N);
     constexpr int P = n_chol(N);
@@ -46,15 +50,9 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     __shared__ __align__(8) uint64_t bar;
 
     const int tid = threadIdx.x;
-    const int64_t w = blockIdx.x;
-    int64_t lo = 0, hi = T;                      // tile t with chunk_off[t] <= w < chunk_off[t+1]
-    while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (chunk_off[mid] <= w) lo = mid;
-        else hi = mid;
-    }
-    const int64_t t = lo;
-    const int64_t c = offsets[t] + (w - chunk_off[t]) * kBwdChunk + tid;
+    const int64_t item = items[blockIdx.x];      // (tile << 32) | chunk, band order
+    const int64_t t = item >> 32;
+    const int64_t c = offsets[t] + (item & 0xffffffffLL) * kBwdChunk + tid;
     const bool active = c < offsets[t + 1];
 
     if (tid == 0) {
@@ -145,27 +143,32 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
         px = fmaf(fabsf(wgt), sqrt_approx(s2), px);
     }
 
-    double* out = accum + e * A;
+    const FxScales fx = fx_scales(bounds, (int64_t)T * tile);
+    unsigned long long* hw = accum + e * A;
+    unsigned long long* lw = hw + Gev * A;
+    unsigned long long* flag = hw + acc_flag(N);
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll
         for (int j = 0; j <= i; ++j) {
             const float2 v = Sp[srow_start(i) + j / 2];
-            atomicAdd(out + tri(i, j), (double)((j & 1) ? v.y : v.x));
+            fx_add(hw + tri(i, j), lw + tri(i, j), flag, (j & 1) ? v.y : v.x, fx.h);
         }
 #pragma unroll
-    for (int i = 0; i < N; ++i) atomicAdd(out + P + i, (double)((i & 1) ? tv2[i / 2].y : tv2[i / 2].x));
-    atomicAdd(out + acc_tail(N), (double)gA0);
-    atomicAdd(out + acc_tail(N) + 1, (double)gA1);
-    atomicAdd(out + acc_tail(N) + 2, (double)gA2);
-    atomicAdd(out + acc_tail(N) + 3, (double)ls);
-    atomicAdd(out + acc_tail(N) + 4, (double)px);
-    atomicAdd(out + acc_tail(N) + 5, (double)tile);
+    for (int i = 0; i < N; ++i) fx_add(hw + P + i, lw + P + i, flag, (i & 1) ? tv2[i / 2].y : tv2[i / 2].x, fx.h);
+    const int T0 = acc_tail(N);
+    fx_add(hw + T0, lw + T0, flag, gA0, fx.g);
+    fx_add(hw + T0 + 1, lw + T0 + 1, flag, gA1, fx.g);
+    fx_add(hw + T0 + 2, lw + T0 + 2, flag, gA2, fx.g);
+    fx_add(hw + T0 + 3, lw + T0 + 3, flag, ls, fx.l);
+    fx_add(hw + T0 + 4, lw + T0 + 4, flag, px, fx.h);
+    atomicAdd(hw + T0 + 5, (unsigned long long)tile);
 }
 
 template <int N>
 int launch_backward(int64_t B, int tile, const float* qrec, const float* rec, int centred, const int64_t* off,
-                    const int32_t* idx, const int64_t* chunk_off, int64_t n_chunks, double* accum, cudaStream_t st) {
+                    const int32_t* idx, const int64_t* items, int64_t n_chunks, int64_t Gev, const uint32_t* bounds,
+                    unsigned long long* accum, cudaStream_t st) {
     const int64_t T = B / tile;
     const size_t smem = sizeof(float) * tile * qrec_floats(N);
     static DeviceOnce attr;
@@ -175,7 +178,7 @@ int launch_backward(int64_t B, int tile, const float* qrec, const float* rec, in
     }
     NDG_REQUIRE(n_chunks <= 0x7fffffffLL, "too many backward work items");
     auto kern = centred ? backward_kernel<N, true> : backward_kernel<N, false>;
-    kern<<<(unsigned)n_chunks, kBwdThreads, smem, st>>>(T, tile, qrec, rec, off, idx, chunk_off, accum);
+    kern<<<(unsigned)n_chunks, kBwdThreads, smem, st>>>(T, tile, qrec, rec, off, idx, items, Gev, bounds, accum);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }
@@ -183,15 +186,16 @@ int launch_backward(int64_t B, int tile, const float* qrec, const float* rec, in
 }  // namespace
 
 extern "C" int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec, int centred,
-                            const int64_t* offsets, const int32_t* idx, const int64_t* chunk_offsets, int64_t n_chunks,
-                            double* accum, void* stream) {
+                            const int64_t* offsets, const int32_t* idx, const int64_t* items, int64_t n_chunks,
+                            int64_t Gev, const uint32_t* bounds, int64_t* accum, void* stream) {
     NDG_REQUIRE(tile >= 1 && tile <= 1024 && B % tile == 0, "tile must be in 1..1024 and divide B");
     if (B == 0 || n_chunks == 0) return NDG_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     switch (n) {
 #define NDG_CASE(NN) \
     case NN:         \
-        return launch_backward<NN>(B, tile, qrec, rec, centred, offsets, idx, chunk_offsets, n_chunks, accum, st);
+        return launch_backward<NN>(B, tile, qrec, rec, centred, offsets, idx, items, n_chunks, Gev, bounds, \
+                                   reinterpret_cast<unsigned long long*>(accum), st);
         NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
         NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
 #undef NDG_CASE

@@ -3,8 +3,8 @@
 //
 // Same contract as the FP32 K7 (ndg_backward.cu): per (tile, candidate) it adds
 //   S' += (w z~) z~^T (lower),  t' += w z~,  gA += g dpred,  loss_share += g ell,  proxy += |w| sqrt(s~)
-// to the float64 accumulators, with w = g h, h = dpred . a, g = 2^-s~, s~ = |z~|^2, in the scaled z~
-// units of the FP32 K7, so the K8 epilogue is shared.
+// to the fixed-point accumulators (deterministic, ndg_common.cuh), with w = g h, h = dpred . a,
+// g = 2^-s~, s~ = |z~|^2, in the scaled z~ units of the FP32 K7, so the K8 epilogue is shared.
 //
 // Why a second kernel: the FP32 K7 keeps one Gaussian per thread with its record (P + 2N + 3 floats)
 // AND its accumulators (P + N + 5) in registers. Past N = 12 that no longer fits in 255 registers;
@@ -63,7 +63,8 @@ template <int N>
 __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
     backward_mma_kernel(int64_t T, int tile, const float* __restrict__ qrec, const float* __restrict__ rec_tc,
                         const int64_t* __restrict__ offsets, const int32_t* __restrict__ idx,
-                        const int64_t* __restrict__ chunk_off, double* __restrict__ accum) {
+                        const int64_t* __restrict__ items, int64_t Gev, const uint32_t* __restrict__ bounds,
+                        unsigned long long* __restrict__ accum) {
     static_assert(N >= 9 && N <= 16, "K7-MMA covers 9 <= N <= 16 (one m16 block of dims)");
     constexpr int QS = qrec_floats(N);
     constexpr int K = tc_k(N);
@@ -77,17 +78,13 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3, odd = gid & 1;
     float* sM = reinterpret_cast<float*>(sQ + tile) + warp * 16 * 17;   // per-warp M^T scratch
-    const int64_t w = blockIdx.x;
-    int64_t lo = 0, hi = T;                   // tile t with chunk_off[t] <= w < chunk_off[t+1]
-    while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (chunk_off[mid] <= w) lo = mid;
-        else hi = mid;
-    }
-    const int64_t t = lo;
-    const int64_t c0 = offsets[t] + (w - chunk_off[t]) * kBwdChunk;
+    const int64_t item = items[blockIdx.x];   // (tile << 32) | chunk, band order (ndg_work_items)
+    const int64_t t = item >> 32;
+    const int64_t c0 = offsets[t] + (item & 0xffffffffLL) * kBwdChunk;
     const int64_t rem = offsets[t + 1] - c0;
     const int n_here = rem < kBwdChunk ? (int)rem : kBwdChunk;
+
+    const FxScales fx = fx_scales(bounds, (int64_t)T * tile);
 
     // ---- the tile's Xhat fragments and (dpred, ell) in shared memory -----------------------------
     const float* qt = qrec + t * tile * QS;
@@ -196,7 +193,9 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
 #pragma unroll
         for (int j = 0; j < kGpw; ++j) {
             if (!live[j]) continue;                       // warp-uniform
-            double* out = accum + e[j] * A;
+            unsigned long long* hw = accum + e[j] * A;
+            unsigned long long* lw = hw + Gev * A;
+            unsigned long long* flag = hw + acc_flag(N);
             // S'[r][c] = P[r][c] + M[r][c] + M[c][r]: M^T through this warp's 16 x 17 scratch
 #pragma unroll
             for (int nb = 0; nb < 2; ++nb)
@@ -210,7 +209,8 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                 for (int v = 0; v < 4; ++v) {
                     const int row = gid + (v >> 1) * 8, colj = nb * 8 + 2 * tig + (v & 1);
                     if (row < N && colj <= row)
-                        atomicAdd(out + tri(row, colj), (double)(S[j][nb][v] + Mx[j][nb][v] + sM[colj * 17 + row]));
+                        fx_add(hw + tri(row, colj), lw + tri(row, colj), flag,
+                               S[j][nb][v] + Mx[j][nb][v] + sM[colj * 17 + row], fx.h);
                 }
             __syncwarp();
             float r[7] = {tz[j][0], tz[j][1], gA[j][0], gA[j][1], gA[j][2], ls[j], px[j]};
@@ -222,16 +222,17 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
 #pragma unroll
             for (int i = 2; i < 7; ++i) r[i] += __shfl_xor_sync(0xffffffffu, r[i], 4);   // both queries of a pair
             if (tig == 0) {
-                atomicAdd(out + P + gid, (double)r[0]);
-                if (gid + 8 < N) atomicAdd(out + P + gid + 8, (double)r[1]);
+                fx_add(hw + P + gid, lw + P + gid, flag, r[0], fx.h);
+                if (gid + 8 < N) fx_add(hw + P + gid + 8, lw + P + gid + 8, flag, r[1], fx.h);
             }
             if (lane == 0) {
-                atomicAdd(out + acc_tail(N), (double)r[2]);
-                atomicAdd(out + acc_tail(N) + 1, (double)r[3]);
-                atomicAdd(out + acc_tail(N) + 2, (double)r[4]);
-                atomicAdd(out + acc_tail(N) + 3, (double)r[5]);
-                atomicAdd(out + acc_tail(N) + 4, (double)r[6]);
-                atomicAdd(out + acc_tail(N) + 5, (double)tile);
+                const int T0 = acc_tail(N);
+                fx_add(hw + T0, lw + T0, flag, r[2], fx.g);
+                fx_add(hw + T0 + 1, lw + T0 + 1, flag, r[3], fx.g);
+                fx_add(hw + T0 + 2, lw + T0 + 2, flag, r[4], fx.g);
+                fx_add(hw + T0 + 3, lw + T0 + 3, flag, r[5], fx.l);
+                fx_add(hw + T0 + 4, lw + T0 + 4, flag, r[6], fx.h);
+                atomicAdd(hw + T0 + 5, (unsigned long long)tile);
             }
         }
     }
@@ -239,14 +240,16 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
 
 template <int N>
 int launch_backward_mma(int64_t B, int tile, const float* qrec, const float* rec_tc, const int64_t* off,
-                        const int32_t* idx, const int64_t* chunk_off, int64_t n_chunks, double* accum, cudaStream_t st) {
+                        const int32_t* idx, const int64_t* items, int64_t n_chunks, int64_t Gev, const uint32_t* bounds,
+                        unsigned long long* accum, cudaStream_t st) {
     const int64_t T = B / tile;
     const size_t smem = sizeof(float4) * ((size_t)tile * 8 + tile) + sizeof(float) * 4 * 16 * 17;
     static DeviceOnce attr;
     if (attr.first())
         cudaFuncSetAttribute(backward_mma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     NDG_REQUIRE(n_chunks <= 0x7fffffffLL, "too many backward work items");
-    backward_mma_kernel<N><<<(unsigned)n_chunks, kThreads, smem, st>>>(T, tile, qrec, rec_tc, off, idx, chunk_off, accum);
+    backward_mma_kernel<N><<<(unsigned)n_chunks, kThreads, smem, st>>>(T, tile, qrec, rec_tc, off, idx, items, Gev, bounds,
+                                                                          accum);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }
@@ -256,8 +259,8 @@ int launch_backward_mma(int64_t B, int tile, const float* qrec, const float* rec
 extern "C" int ndg_backward_mma_supported(int n) { return n >= 9 && n <= 16; }
 
 extern "C" int ndg_backward_mma(int n, int64_t B, int tile, const float* qrec, const float* rec_tc,
-                                const int64_t* offsets, const int32_t* idx, const int64_t* chunk_offsets,
-                                int64_t n_chunks, double* accum, void* stream) {
+                                const int64_t* offsets, const int32_t* idx, const int64_t* items,
+                                int64_t n_chunks, int64_t Gev, const uint32_t* bounds, int64_t* accum, void* stream) {
     NDG_REQUIRE(tile >= 8 && tile <= 1024 && tile % 8 == 0 && B % tile == 0,
                 "K7-MMA needs tile in 8..1024, a multiple of 8, dividing B");
     if (B == 0 || n_chunks == 0) return NDG_OK;
@@ -265,7 +268,8 @@ extern "C" int ndg_backward_mma(int n, int64_t B, int tile, const float* qrec, c
     switch (n) {
 #define NDG_CASE(NN) \
     case NN:         \
-        return launch_backward_mma<NN>(B, tile, qrec, rec_tc, offsets, idx, chunk_offsets, n_chunks, accum, st);
+        return launch_backward_mma<NN>(B, tile, qrec, rec_tc, offsets, idx, items, n_chunks, Gev, bounds, \
+                                       reinterpret_cast<unsigned long long*>(accum), st);
         NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
 #undef NDG_CASE
         default:

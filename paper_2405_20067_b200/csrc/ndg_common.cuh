@@ -56,15 +56,79 @@ __host__ __device__ constexpr int tc_rec_floats(int n) { return n * tc_k(n) + 4;
 // Backward query record (float32): x[N] | dpred[3] | ell, produced by the fused forward+loss.
 __host__ __device__ constexpr int qrec_floats(int n) { return pad4(n + 4); }
 
-// Accumulators per evaluated Gaussian (float64): S'[P] | t'[N] | spare | gA[3] | loss_share | proxy |
-// pairs in the scaled z~ units with coefficient +g*h (the epilogue applies -1/C^2, -1/C, 1/C).
-// The tensor-core backward fills the first P + N + 1 slots with the x-space moments
-// M = sum w xhat xhat^T (xhat = [x - 1/2; 1], packed lower triangle of the (N+1)^2 matrix, which is
-// exactly quad[P] | lin[N] | const) and ndg_moments_to_zspace turns them into S' | t' in place.
+// Accumulators per evaluated Gaussian: S'[P] | t'[N] | flag | gA[3] | loss_share | proxy | pairs, in the
+// scaled z~ units with coefficient +g*h (the epilogue applies -1/C^2, -1/C, 1/C). The backward adds
+// into them as two int64 fixed-point words per slot (see "deterministic reduction" below);
+// ndg_acc_dequant turns them into float64 in place for the K8 epilogue. `flag` is nonzero when a
+// partial was non-finite or outside its bound (the epilogue then sees NaN -> NonFiniteGradientError).
+__host__ __device__ constexpr int acc_flag(int n) { return n_chol(n) + n; }
 __host__ __device__ constexpr int acc_tail(int n) { return n_chol(n) + n + 1; }
 __host__ __device__ constexpr int acc_doubles(int n) { return acc_tail(n) + 3 + kNumStats; }
 
+// Backward work items in band order (ndg_work_items): bands of kBand tiles run chunk-major.
+constexpr int kBand = 512;
+
 constexpr double kC = 0.84932180028801907;      // sqrt(0.5 * log2(e))
+
+}  // namespace ndg
+
+// ---------------------------------------------------------------------------------------------
+// Deterministic cross-tile reduction of the backward.
+//
+// Every per-(tile, candidate) float32 partial v of accumulator slot j is added to TWO int64 words,
+//   hi[j] += rint(x),  lo[j] += rint((x - rint(x)) * 2^40),   x = v * s_c,
+// with s_c = 2^(62 - e_c) a power of two from an a-priori bound U_c = 2^e_c (rounded up) on the sum of
+// |v| over every partial of the slot's class c. Integer addition is associative, so the two sums --
+// and the float64 value hi / s_c + lo / (s_c 2^40) that ndg_acc_dequant makes of them -- are the same
+// whatever order the tiles finish in: gradients and checkpoints are bitwise reproducible. The
+// quantum is U_c * 2^-102, far below the float32 rounding of the per-tile partials themselves.
+// Bounds per pair (exact arithmetic, x2 margin for float32 rounding; at most B pairs per Gaussian):
+//   h-class (S', t', proxy): g z~_i z~_j <= max x 2^-x = 0.531, g |z~_i| and g sqrt(s~) <= 0.515, so
+//             |term| <= 0.54 |h| with |h| = |dpred . a| <= H * Amax;
+//   gA:       g |dpred_c| <= Dmax;     loss share: g ell <= Lmax;     pairs: exact integer counts.
+// H, Dmax, Lmax (over the step's queries) and Amax (over live Gaussians) come from ndg_bwd_bounds as
+// float bit patterns (uint32 atomicMax of non-negative floats; NaN sorts above +inf, so a non-finite
+// input poisons the scale and every partial is flagged).
+// ---------------------------------------------------------------------------------------------
+namespace ndg {
+
+struct FxScales {
+    double h, g, l;
+};
+
+__device__ __forceinline__ double fx_scale_for(double U) {
+    if (U == 0.0) return 1.0;                      // the class is identically zero
+    if (!(U > 0.0) || isinf(U)) return __longlong_as_double(0x7ff8000000000000LL);   // NaN: flag everything
+    int ex;
+    frexp(U, &ex);                                 // U = m 2^ex, m in [0.5, 1): U <= 2^ex
+    int s = 62 - ex;
+    s = s > 960 ? 960 : (s < -960 ? -960 : s);
+    return ldexp(1.0, s);
+}
+
+__device__ __forceinline__ FxScales fx_scales(const uint32_t* __restrict__ bnd, int64_t B) {
+    const double H = __uint_as_float(bnd[0]), D = __uint_as_float(bnd[1]), Lm = __uint_as_float(bnd[2]),
+                 Am = __uint_as_float(bnd[3]);
+    const double nb = 2.0 * (double)B;
+    return FxScales{fx_scale_for(nb * 0.54 * H * Am), fx_scale_for(nb * D), fx_scale_for(nb * Lm)};
+}
+
+constexpr double kFxLo = 1099511627776.0;          // 2^40: the lo word's extra resolution
+
+__device__ __forceinline__ void fx_add(unsigned long long* hi, unsigned long long* lo, unsigned long long* flag,
+                                       float v, double sc) {
+    if (v == 0.f) return;
+    const double x = (double)v * sc;
+    if (!(fabs(x) < 4611686018427387904.0)) {      // non-finite, or past 2^62: never silently wrong
+        atomicOr(flag, 1ull);
+        return;
+    }
+    const double xh = rint(x);
+    const long long qh = (long long)xh;
+    if (qh) atomicAdd(hi, (unsigned long long)qh);
+    const long long ql = __double2ll_rn((x - xh) * kFxLo);
+    if (ql) atomicAdd(lo, (unsigned long long)ql);
+}
 
 }  // namespace ndg
 

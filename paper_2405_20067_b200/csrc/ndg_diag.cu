@@ -188,6 +188,57 @@ int launch_loss_f64(int G, int amp_mode, int M, const double* params, const doub
     return NDG_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Float64 backward pair loop (gradcheck's analytic side; not on the training path):
+// thread per evaluated Gaussian over every query (culling off), same sufficient statistics and z~
+// scaling as K7 (S' = sum w z~ z~^T, t' = sum w z~, gA, loss share, proxy, pairs with z~ = C z,
+// g = 2^-|z~|^2, w = g dpred . a) but all in float64, written (not added) to accum[Gev][A] for the
+// K8 epilogue. So the analytic gradient can be held to SPEC.md:572's per-coordinate bar.
+// ---------------------------------------------------------------------------------------------
+template <int N>
+__global__ void backward_f64_kernel(int64_t G, int64_t Gev, int amp_mode, const float* __restrict__ params,
+                                    const float* __restrict__ child, const double* __restrict__ mean64,
+                                    const double* __restrict__ chol64, const uint8_t* __restrict__ eflags, int64_t B,
+                                    const float* __restrict__ queries, const double* __restrict__ dpred,
+                                    const double* __restrict__ ell, double* __restrict__ accum) {
+    constexpr int P = n_chol(N), A = acc_doubles(N), T0 = acc_tail(N), R = raw_floats(N);
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= Gev) return;
+    double* acc = accum + e * A;
+    for (int j = 0; j < A; ++j) acc[j] = 0.0;
+    if ((eflags[e] & 3) != 1) return;
+    const float* row = e < G ? params + e * R : child + (e - G) * R;
+    const double ampr = (double)row[N + P + 3];
+    const double alpha = amp_mode == NDG_BRIGHTNESS ? exp(ampr) : gc_sigmoid(ampr);
+    double a[3], L[P], m[N];
+    for (int ch = 0; ch < 3; ++ch) a[ch] = alpha * gc_sigmoid((double)row[N + P + ch]);
+    for (int t = 0; t < P; ++t) L[t] = chol64[e * P + t];
+    for (int r = 0; r < N; ++r) m[r] = mean64[e * N + r];
+    for (int64_t q = 0; q < B; ++q) {
+        double z[N], s = 0.0;
+        for (int r = 0; r < N; ++r) {
+            double v = (double)queries[q * N + r] - m[r];
+            for (int k = 0; k < r; ++k) v -= L[tri(r, k)] * z[k];
+            z[r] = v / L[tri(r, r)];
+        }
+        for (int r = 0; r < N; ++r) {
+            z[r] *= kC;
+            s += z[r] * z[r];
+        }
+        const double g = exp2(-s);
+        const double* dp = dpred + q * 3;
+        const double w = g * (dp[0] * a[0] + dp[1] * a[1] + dp[2] * a[2]);
+        for (int i = 0; i < N; ++i) {
+            for (int j = 0; j <= i; ++j) acc[tri(i, j)] += w * z[i] * z[j];
+            acc[P + i] += w * z[i];
+        }
+        for (int ch = 0; ch < 3; ++ch) acc[T0 + ch] += g * dp[ch];
+        if (ell) acc[T0 + 3] += g * ell[q];
+        acc[T0 + 4] += fabs(w) * sqrt(s);
+        acc[T0 + 5] += 1.0;
+    }
+}
+
 }  // namespace
 
 extern "C" int ndg_active_mask(int n, int64_t B, int tile, const float* queries, const double* mean64,
@@ -225,4 +276,28 @@ extern "C" int ndg_loss_f64(int n, int G, int amp_mode, int M, const double* par
         default:
             return NDG_ERR_UNSUPPORTED_DIMS;
     }
+}
+
+extern "C" int ndg_backward_f64(int n, int64_t G, int64_t Gev, int amp_mode, const float* params, const float* child,
+                                const double* mean64, const double* chol64, const uint8_t* eflags, int64_t B,
+                                const float* queries, const double* dpred, const double* ell, double* accum,
+                                void* stream) {
+    NDG_REQUIRE(Gev == G || Gev == 2 * G, "Gev must be G or 2G");
+    if (Gev == 0) return NDG_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const unsigned grid = (unsigned)((Gev + 63) / 64);
+    switch (n) {
+#define NDG_CASE(NN)                                                                                            \
+    case NN:                                                                                                    \
+        backward_f64_kernel<NN><<<grid, 64, 0, st>>>(G, Gev, amp_mode, params, child, mean64, chol64, eflags, B, \
+                                                     queries, dpred, ell, accum);                               \
+        break;
+        NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
+        NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
+#undef NDG_CASE
+        default:
+            return NDG_ERR_UNSUPPORTED_DIMS;
+    }
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
 }

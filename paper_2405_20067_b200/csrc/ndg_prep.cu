@@ -445,6 +445,146 @@ extern "C" int ndg_scan_counts(int64_t T, const int64_t* counts, int64_t* offset
 }
 
 // ---------------------------------------------------------------------------------------------
+// K7 work items in band order. One CTA per band of kBand tiles writes that band's items
+// (t << 32 | c) into items[chunk_offsets[b0] .. chunk_offsets[b1]): the first cmin chunks (cmin = the
+// fewest any tile of the band has) chunk-major -- all of the band's tiles on chunk 0, then on chunk 1 --
+// so the CTAs in flight at one time share the same Gaussians' records and accumulators in L2 (dense
+// regimes: every tile's list is almost the whole mixture), the remaining chunks tile-major after them.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) work_items_kernel(int64_t T, const int64_t* __restrict__ chunk_off,
+                                                         int64_t* __restrict__ items) {
+    __shared__ int64_t s_ex[kBand + 1];
+    __shared__ int64_t s_min;
+    const int64_t b0 = (int64_t)blockIdx.x * kBand, b1 = imin64(b0 + kBand, T);
+    const int nb = (int)(b1 - b0);
+    if (threadIdx.x == 0) s_min = INT64_MAX;
+    __syncthreads();
+    int64_t mn = INT64_MAX;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) mn = min(mn, chunk_off[b0 + i + 1] - chunk_off[b0 + i]);
+    atomicMin(reinterpret_cast<unsigned long long*>(&s_min), (unsigned long long)mn);
+    __syncthreads();
+    const int64_t cmin = s_min;
+    if (threadIdx.x == 0) {                       // exclusive prefix of the extra chunks per tile
+        int64_t a = 0;
+        for (int i = 0; i < nb; ++i) {
+            s_ex[i] = a;
+            a += chunk_off[b0 + i + 1] - chunk_off[b0 + i] - cmin;
+        }
+        s_ex[nb] = a;
+    }
+    __syncthreads();
+    const int64_t base = chunk_off[b0], head = cmin * nb, total = head + s_ex[nb];
+    for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
+        int64_t t, c;
+        if (i < head) {
+            c = i / nb;
+            t = b0 + i % nb;
+        } else {
+            const int64_t j = i - head;
+            int lo = 0, hi = nb;                  // s_ex[lo] <= j < s_ex[lo + 1]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_ex[mid] <= j) lo = mid;
+                else hi = mid;
+            }
+            t = b0 + lo;
+            c = cmin + (j - s_ex[lo]);
+        }
+        items[base + i] = (t << 32) | c;
+    }
+}
+
+extern "C" int ndg_work_items(int64_t T, const int64_t* chunk_offsets, int64_t* items, void* stream) {
+    if (T <= 0) return NDG_OK;
+    work_items_kernel<<<(unsigned)((T + kBand - 1) / kBand), 256, 0, as_stream(stream)>>>(T, chunk_offsets, items);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Bounds of the deterministic backward reduction (ndg_common.cuh): H = max_q sum_c |dpred_c|,
+// Dmax = max_q,c |dpred_c|, Lmax = max_q ell over the step's query records, Amax = max |a_c| over live
+// Gaussians -- as float bit patterns (uint32 atomicMax of non-negative values; `bounds` zeroed by the
+// caller). Order-independent, so the scales every K7 launch derives from them are deterministic.
+// ---------------------------------------------------------------------------------------------
+__global__ void bwd_bounds_kernel(int n, int64_t B, const float* __restrict__ qrec, int64_t Gev,
+                                  const float* __restrict__ rec, const uint8_t* __restrict__ eflags,
+                                  uint32_t* __restrict__ bounds) {
+    const int QS = qrec_floats(n), RS = rec_floats(n), A0 = rec_a(n);
+    uint32_t h = 0, d = 0, l = 0, am = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < B; q += stride) {
+        const float* r = qrec + q * QS + n;
+        const float a0 = fabsf(r[0]), a1 = fabsf(r[1]), a2 = fabsf(r[2]);
+        h = max(h, __float_as_uint(fabsf(a0 + a1 + a2)));
+        d = max(d, max(__float_as_uint(a0), max(__float_as_uint(a1), __float_as_uint(a2))));
+        l = max(l, __float_as_uint(fabsf(r[3])));
+    }
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < Gev; e += stride) {
+        if ((eflags[e] & 3) != 1) continue;       // live, not degenerate
+        const float* r = rec + e * RS + A0;
+        am = max(am, max(__float_as_uint(fabsf(r[0])), max(__float_as_uint(fabsf(r[1])), __float_as_uint(fabsf(r[2])))));
+    }
+    h = __reduce_max_sync(0xffffffffu, h);
+    d = __reduce_max_sync(0xffffffffu, d);
+    l = __reduce_max_sync(0xffffffffu, l);
+    am = __reduce_max_sync(0xffffffffu, am);
+    if ((threadIdx.x & 31) == 0) {
+        if (h) atomicMax(bounds + 0, h);
+        if (d) atomicMax(bounds + 1, d);
+        if (l) atomicMax(bounds + 2, l);
+        if (am) atomicMax(bounds + 3, am);
+    }
+}
+
+extern "C" int ndg_bwd_bounds(int n, int64_t B, const float* qrec, int64_t Gev, const float* rec,
+                              const uint8_t* eflags, uint32_t* bounds, void* stream) {
+    if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
+    bwd_bounds_kernel<<<148 * 4, 256, 0, as_stream(stream)>>>(n, B, qrec, Gev, rec, eflags, bounds);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fixed point -> float64 accumulators, in place over the hi words (acc = [2][Gev][A] int64 -> the
+// first Gev * A words become float64). A flagged Gaussian gets NaN in every slot (its flag slot's
+// output is NaN too, so a thread reading the flag after it was overwritten still sees nonzero bits).
+// ---------------------------------------------------------------------------------------------
+__global__ void acc_dequant_kernel(int n, int64_t Gev, int64_t B, const uint32_t* __restrict__ bounds,
+                                   long long* __restrict__ acc) {
+    const int A = acc_doubles(n), F = acc_flag(n), T0 = acc_tail(n);
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= Gev * A) return;
+    const int j = (int)(i % A);
+    const int64_t e = i / A;
+    const FxScales fx = fx_scales(bounds, B);
+    const long long hi = acc[i], lo = acc[Gev * A + i];
+    const bool bad = acc[e * A + F] != 0;
+    double v;
+    if (bad) {
+        v = __longlong_as_double(0x7ff8000000000000LL);
+    } else if (j == F) {
+        v = 0.0;
+    } else if (j == T0 + 5) {
+        v = (double)hi;                                  // pairs: exact count
+    } else {
+        const double sc = (j < F || j == T0 + 4) ? fx.h : (j < T0 + 3 ? fx.g : fx.l);
+        v = (double)hi / sc + (double)lo / (sc * kFxLo);
+    }
+    reinterpret_cast<double*>(acc)[i] = v;
+}
+
+extern "C" int ndg_acc_dequant(int n, int64_t Gev, int64_t B, const uint32_t* bounds, int64_t* acc, void* stream) {
+    if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
+    const int64_t total = Gev * acc_doubles(n);
+    if (total == 0) return NDG_OK;
+    acc_dequant_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(
+        n, Gev, B, bounds, reinterpret_cast<long long*>(acc));
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
 // K4c compaction: CTA per tile; block prefix scan of per-word popcounts, then each thread writes
 // the ascending indices of its word's set bits.
 // ---------------------------------------------------------------------------------------------
@@ -515,6 +655,45 @@ __global__ void loss_finalize_kernel(int64_t T, const double* __restrict__ part,
         __syncthreads();
     }
     if (threadIdx.x == 0) *loss = s[0];
+}
+
+// ---------------------------------------------------------------------------------------------
+// Standalone loss_rel_l2 for the module-level API (the training step fuses it into
+// K5): per 256-query block a float64 partial (fixed-order tree), then ndg_loss_finalize. dpred (may be
+// NULL) = 2 (p - t) / (p^2 + eps) / (3 n_total), the gradient with the denominator detached (:291).
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) loss_rel_l2_kernel(int64_t B, const float* __restrict__ pred,
+                                                          const float* __restrict__ target, float eps, int64_t n_total,
+                                                          float* __restrict__ dpred, double* __restrict__ part) {
+    __shared__ double s[256];
+    const int64_t b = blockIdx.x * 256LL + threadIdx.x;
+    double l = 0.0;
+    if (b < B) {
+        const double inv = 1.0 / (3.0 * (double)n_total);
+        for (int c = 0; c < 3; ++c) {
+            const double p = pred[b * 3 + c], d = p - (double)target[b * 3 + c], den = p * p + (double)eps;
+            l += d * d / den;
+            if (dpred) dpred[b * 3 + c] = (float)(2.0 * d / den * inv);
+        }
+        l *= inv;
+    }
+    s[threadIdx.x] = l;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+
+extern "C" int ndg_loss_rel_l2(int64_t B, const float* pred, const float* target, float eps, int64_t n_total,
+                               float* dpred, double* loss_partial, void* stream) {
+    NDG_REQUIRE(eps > 0.f && n_total >= 1, "eps > 0 and n_total >= 1 required (SPEC.md:255)");
+    if (B == 0) return NDG_OK;
+    loss_rel_l2_kernel<<<(unsigned)((B + 255) / 256), 256, 0, as_stream(stream)>>>(B, pred, target, eps, n_total,
+                                                                                    dpred, loss_partial);
+    NDG_CHECK_LAUNCH();
+    return NDG_OK;
 }
 
 extern "C" int ndg_loss_finalize(int64_t T, const double* loss_partial, double* loss, void* stream) {

@@ -157,13 +157,23 @@ class ShadingToyTarget:
         return (alb * shade * 0.6 + 0.4 * lobe).to(torch.float32)
 
 
-def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, generator, device):
+def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, generator, device, rank: int = 0,
+                 world: int = 1):
     """SPEC.md:440-448 on the device: fresh uniform queries, stable-sorted by the first (position)
-    dimension into contiguous tiles, exact targets. batch_size must be a multiple of tile_size."""
+    dimension into contiguous tiles, exact targets. batch_size must be a multiple of tile_size.
+
+    Data-parallel (world > 1): every rank draws the same GLOBAL batch from identically seeded
+    generators and keeps its strided tiles (global tile i -> rank i mod world, parallel.shard_tiles),
+    evaluating the target only there -- so the union over ranks is exactly the 1-GPU batch and the
+    summed gradients equal the 1-GPU step's."""
     import torch
     if batch_size % tile_size:
         raise ValueError("batch_size must be a multiple of tile_size (SPEC.md:441)")
     q = torch.rand(batch_size, n_dims, generator=generator, device=device)
     order = torch.sort(q[:, 0], stable=True).indices
-    q = q[order].contiguous()
+    q = q[order]
+    if world > 1:
+        T = batch_size // tile_size
+        q = q.view(T, tile_size, n_dims)[rank::world].reshape(-1, n_dims)
+    q = q.contiguous()
     return q, target(q).contiguous()

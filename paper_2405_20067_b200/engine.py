@@ -11,8 +11,8 @@ gmm-core, culling and grad modules, each enqueued on the current CUDA stream thr
        ndg_forward       (FP32-pipe K5: ill-conditioned mixtures, tiles > 256, NDG_FORWARD=fp32)
     K7 ndg_backward      backward pair loop, FP32 pipe (N <= 14)
        ndg_backward_mma  (warp-MMA pair loop: N >= 15, or NDG_BACKWARD=mma for N >= 9)
-       ndg_backward_tc   (opt-in NDG_BACKWARD=tc: tcgen05 z-GEMM + moments, N <= 12)
-    K7b ndg_moments_to_zspace  x-space moments -> S', t' (tcgen05 K7 only)
+       (+ ndg_bwd_bounds / ndg_work_items before, ndg_acc_dequant after: the deterministic
+        fixed-point reduction of SPEC.md:294, and the band order of the work items)
     K8 ndg_epilogue      backward tail, raw-parameter chain rule
     K9 ndg_adam          adam_step
 
@@ -100,6 +100,12 @@ class EvalRecords:
         mx, ss, cnt = self.tc_cond_host
         return math.sqrt(ss / cnt) if cnt > 0 else 0.0
 
+    def tc_peak(self) -> float:
+        """max over live Gaussians of B_e: the worst single Gaussian's conditioning."""
+        if self.tc_cond_host is None:
+            self.tc_conditioning()
+        return float(self.tc_cond_host[0]) if self.tc_cond_host is not None else float("inf")
+
 
 @dataclass
 class ProjectedBounds:
@@ -139,12 +145,20 @@ class CandidateLists:
 @dataclass
 class GradientBuffer:
     """Raw-layout gradients of parents and children plus the density-control
-    statistics, all views into ONE flat float32 buffer so a multi-GPU step needs one allreduce."""
+    statistics, all views into ONE flat float32 buffer so a multi-GPU step needs one allreduce.
+    Layout [params | stats | scalars | child]: without live children the child block is all zero
+    and the step reduces only the prefix `reduced()` (half the bytes at cfg5)."""
     flat: torch.Tensor
     params: torch.Tensor      # [G, R]
     child: torch.Tensor       # [G, R]
     stats: torch.Tensor       # [Gev, 3]: loss share, gradient proxy, pairs
     scalars: torch.Tensor     # [2]: loss, total pairs (filled by the caller that reduces)
+    children_live: bool = False
+
+    def reduced(self) -> torch.Tensor:
+        """The part of `flat` the step's allreduce must sum (the child block only when live)."""
+        n = self.flat.numel() - (0 if self.children_live else self.child.numel())
+        return self.flat[:n]
 
 
 @dataclass
@@ -162,9 +176,10 @@ def alloc_gradients(G: int, Gev: int, n: int, device) -> GradientBuffer:
     flat = torch.zeros(2 * G * R + 3 * Gev + 2, dtype=torch.float32, device=device)
     o = 0
     gp = flat[o:o + G * R].view(G, R); o += G * R
-    gc = flat[o:o + G * R].view(G, R); o += G * R
     st = flat[o:o + 3 * Gev].view(Gev, 3); o += 3 * Gev
-    return GradientBuffer(flat, gp, gc, st, flat[o:o + 2])
+    sc = flat[o:o + 2]; o += 2
+    gc = flat[o:o + G * R].view(G, R)
+    return GradientBuffer(flat, gp, gc, st, sc, Gev == 2 * G)
 
 
 def decode_status(st, G: int, n: int) -> int:
@@ -208,15 +223,12 @@ class HotPath:
         if self.forward_impl == "tc" and self.tile > 256:
             self.forward_impl = "fp32"      # the tcgen05 K5 covers tiles of up to two 128-query halves
         # K7 implementation: "auto" (default) = warp-MMA K7 for N >= MMA_MIN_N, else the FP32-pipe pair
-        # loop; "fp32" / "mma" force one (both per-step guarded); "tc" = tcgen05 z-GEMM + moments GEMM
-        # (N <= 12, opt-in: no faster and only marginally within 1e-4)
+        # loop; "fp32" / "mma" force one (both per-step guarded)
         bwd = backward or os.environ.get("NDG_BACKWARD", "auto")
-        if bwd not in ("auto", "tc", "fp32", "mma"):
-            raise ValueError("backward must be 'auto', 'fp32', 'mma' or 'tc'")
+        if bwd not in ("auto", "fp32", "mma"):
+            raise ValueError("backward must be 'auto', 'fp32' or 'mma'")
         lib = K.load()
-        if bwd == "tc":
-            bwd = "tc" if lib.ndg_backward_tc_supported(self.n) else "fp32"
-        elif bwd == "auto":
+        if bwd == "auto":
             bwd = "mma" if self.n >= self.MMA_MIN_N else "fp32"
         if bwd == "mma" and not (lib.ndg_backward_mma_supported(self.n) and self.tile % 8 == 0):
             bwd = "fp32"
@@ -270,16 +282,21 @@ class HotPath:
     # at 35, sigma 0.02 at 256 (parity 4.4e-5), the N=1 sigma 8e-4 mixture of tests/test_gpu_fuzz.py
     # at 842 (2.3e-4, out of tolerance). The moments K7 loses ~B^2 and is held to broad mixtures.
     TC_FORWARD_MAX_BOUND = 200.0      # RMS of B_e; error ~2e-7 * RMS (measured 4.4e-5 @ 256, 2.3e-4 @ 842)
-    TC_BACKWARD_MAX_BOUND = 20.0      # moments K7: error ~8e-8 * RMS^2 (9.7e-5 vs the FP32 K7 @ 35)
+    # ... and the worst single Gaussian: the error is per Gaussian (~2e-7 B_e on its own terms), so a few
+    # very sharp Gaussians among broad ones barely move the RMS but would carry their own contributions
+    # past the bar; past this peak the step runs the FP32 kernels (centred records, exact near the
+    # Gaussian). cfg2's synthetic mixture peaks at ~520 (RMS 35), cfg4's at ~390.
+    TC_FORWARD_PEAK_BOUND = 1000.0
 
     # The FP32 kernels' first term rho x + nb2 cancels like the z-GEMM (error ~1.4e-7 * RMS(B), e.g.
     # 1.45e-4 at RMS 1022 for the sigma 7e-4 mixture of tests/test_gpu_fuzz.py); past this bound they
     # run on centred records, z = rho ((x - m_hi) - m_lo), which loses nothing near the Gaussian.
     FP32_CENTRE_BOUND = 150.0
+    FP32_CENTRE_PEAK_BOUND = 1000.0     # any single Gaussian past this also selects centred records
 
     def centred_records(self, recs: EvalRecords):
         """K1c records (or None) for the FP32 K5 / K7 of this step."""
-        if recs.tc_conditioning() <= self.FP32_CENTRE_BOUND:
+        if recs.tc_conditioning() <= self.FP32_CENTRE_BOUND and recs.tc_peak() <= self.FP32_CENTRE_PEAK_BOUND:
             return None
         if recs.rec_c is None:
             recs.rec_c = torch.empty_like(recs.rec)
@@ -289,11 +306,8 @@ class HotPath:
     def forward_tc_ok(self, recs: EvalRecords) -> bool:
         """Whether this step's K5 runs on the tensor cores (else the FP32-pipe K5, same contract)."""
         return (self.forward_impl == "tc" and recs.rec_tc is not None
-                and recs.tc_conditioning() <= self.TC_FORWARD_MAX_BOUND)
-
-    def backward_tc_ok(self, recs: EvalRecords) -> bool:
-        return (self.backward_impl == "tc" and recs.rec_tc is not None
-                and recs.tc_conditioning() <= self.TC_BACKWARD_MAX_BOUND)
+                and recs.tc_conditioning() <= self.TC_FORWARD_MAX_BOUND
+                and recs.tc_peak() <= self.TC_FORWARD_PEAK_BOUND)
 
     # The warp-MMA K7 forms z~ with the K5 z-GEMM (same records, same error ~2e-7 * RMS(B)), so it
     # shares the tensor-core forward's bound. Its cost does not depend on N (dims pad to one m16
@@ -303,12 +317,11 @@ class HotPath:
 
     def backward_mma_ok(self, recs: EvalRecords) -> bool:
         return (self.backward_impl == "mma" and recs.rec_tc is not None
-                and recs.tc_conditioning() <= self.TC_FORWARD_MAX_BOUND)
+                and recs.tc_conditioning() <= self.TC_FORWARD_MAX_BOUND
+                and recs.tc_peak() <= self.TC_FORWARD_PEAK_BOUND)
 
     def backward_kernel_impl(self, recs: EvalRecords) -> str:
-        """Which K7 this step runs: "tc", "mma" or "fp32"."""
-        if self.backward_tc_ok(recs):
-            return "tc"
+        """Which K7 this step runs: "mma" or "fp32"."""
         return "mma" if self.backward_mma_ok(recs) else "fp32"
 
     # -- K2 --------------------------------------------------------------------------------
@@ -422,27 +435,29 @@ class HotPath:
 
     # -- K7 + K8 ---------------------------------------------------------------------------
     def backward(self, mix: Mixture, recs: EvalRecords, cl: CandidateLists, qrec, grads: GradientBuffer):
+        """K7 + K8. The cross-tile sums are exact int64 fixed point (two words per accumulator, scales
+        from ndg_bwd_bounds), so gradients do not depend on the order work items finish."""
         B = int(qrec.shape[0])
-        accum = torch.zeros(recs.Gev, self.L["acc"], dtype=torch.float64, device=self.device)
+        T, Gev, A = B // self.tile, recs.Gev, self.L["acc"]
+        acc = torch.zeros(2, Gev, A, dtype=torch.int64, device=self.device)
+        bounds = torch.zeros(4, dtype=torch.int32, device=self.device)
+        K.call("ndg_bwd_bounds", self.n, B, _p(qrec), Gev, _p(recs.rec), _p(recs.eflags), _p(bounds), _stream())
+        items = torch.empty(max(cl.n_chunks, 1), dtype=torch.int64, device=self.device)
+        K.call("ndg_work_items", T, _p(cl.chunk_offsets), _p(items), _stream())
         self._ev("backward", 0)
         self.last_backward_impl = self.backward_kernel_impl(recs)
         if self.last_backward_impl == "mma":
             K.call("ndg_backward_mma", self.n, B, self.tile, _p(qrec), _p(recs.rec_tc), _p(cl.offsets), _p(cl.idx),
-                   _p(cl.chunk_offsets), cl.n_chunks, _p(accum), _stream())
-            self._ev("backward", 1)
-        elif self.last_backward_impl == "tc":
-            K.call("ndg_backward_tc", self.n, B, self.tile, _p(qrec), _p(recs.rec_tc), _p(cl.offsets), _p(cl.idx),
-                   _p(accum), _stream())
-            self._ev("backward", 1)
-            K.call("ndg_moments_to_zspace", self.n, recs.Gev, _p(recs.mean64), _p(recs.chol64), _p(recs.eflags),
-                   _p(accum), _stream())
+                   _p(items), cl.n_chunks, Gev, _p(bounds), _p(acc), _stream())
         else:
             rc = self.centred_records(recs)
             self.last_centred = rc is not None
             K.call("ndg_backward", self.n, B, self.tile, _p(qrec), _p(recs.rec if rc is None else rc),
-                   int(rc is not None), _p(cl.offsets), _p(cl.idx),
-                   _p(cl.chunk_offsets), cl.n_chunks, _p(accum), _stream())
-            self._ev("backward", 1)
+                   int(rc is not None), _p(cl.offsets), _p(cl.idx), _p(items), cl.n_chunks, Gev, _p(bounds),
+                   _p(acc), _stream())
+        self._ev("backward", 1)
+        K.call("ndg_acc_dequant", self.n, Gev, B, _p(bounds), _p(acc), _stream())
+        accum = acc[0].view(torch.float64)
         K.call("ndg_epilogue", self.n, mix.G, recs.Gev, mix.amp_mode, _p(mix.params), _p(mix.child), _p(mix.flags),
                _p(recs.eflags), _p(recs.chol64), _p(accum), _p(grads.params), _p(grads.child), _p(grads.stats),
                _p(self.status), _stream())
@@ -458,15 +473,21 @@ class HotPath:
 
     # -- whole step ------------------------------------------------------------------------
     def fwd_bwd(self, mix: Mixture, queries, targets, *, cull: bool = True, n_total=None, grads=None,
-                allreduce=None, check: bool = True) -> StepResult:
+                allreduce=None, check: bool = True, candidates: CandidateLists | None = None) -> StepResult:
         """One culled forward + loss + backward pass (SPEC.md:329 minus the optimizer step).
 
         `allreduce(flat)` -- when given -- sums the flat gradient buffer across ranks (one NCCL
-        collective) before the status / loss read-back."""
+        collective) before the status / loss read-back. `candidates` -- when given --
+        are the per-tile active sets to use (SPEC.md:263's "active sets per tile"), e.g. from cull()."""
         self.reset_status()
         recs = self.activate(mix)
         T = int(queries.shape[0]) // self.tile
-        if cull:
+        if candidates is not None:
+            if candidates.T != T:
+                raise ValueError("candidate lists do not match the batch's tile count")
+            cl = candidates
+            recs.tc_conditioning()                       # the read-back cull() would have carried
+        elif cull:
             pb = self.project(recs)
             tb = self.tile_bounds(queries)
             cl = self.cull(tb, pb)
@@ -479,8 +500,9 @@ class HotPath:
         self.backward(mix, recs, cl, qrec, grads)
         grads.scalars[0] = loss[0].to(torch.float32)
         grads.scalars[1] = float(cl.n_pairs_tiles * self.tile)
+        grads.children_live = recs.Gev == 2 * mix.G
         if allreduce is not None:
-            allreduce(grads.flat)
+            allreduce(grads.reduced())
         host = torch.cat([self.status, loss.view(torch.int64)]).cpu()
         n_deg = self.check_status(mix, host[:4]) if check else 0
         loss_v = float(host[4:5].view(torch.float64)[0]) if allreduce is None else float(grads.scalars[0])

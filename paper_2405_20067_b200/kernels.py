@@ -39,13 +39,15 @@ SIGNATURES = {
     "ndg_forward": [_I, _L, _I, _P, _P, _P, _I, _P, _P, _F, _L, _P, _P, _P, _P],
     "ndg_centre_records": [_I, _L, _P, _P, _P, _P],
     "ndg_loss_finalize": [_L, _P, _P, _P],
-    "ndg_backward": [_I, _L, _I, _P, _P, _I, _P, _P, _P, _L, _P, _P],
-    "ndg_backward_tc_supported": [_I],
-    "ndg_backward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _P],
-    "ndg_moments_to_zspace": [_I, _L, _P, _P, _P, _P, _P],
+    "ndg_loss_rel_l2": [_L, _P, _P, _F, _L, _P, _P, _P],
+    "ndg_work_items": [_L, _P, _P, _P],
+    "ndg_bwd_bounds": [_I, _L, _P, _L, _P, _P, _P, _P],
+    "ndg_backward": [_I, _L, _I, _P, _P, _I, _P, _P, _P, _L, _L, _P, _P, _P],
+    "ndg_acc_dequant": [_I, _L, _L, _P, _P, _P],
     "ndg_backward_mma_supported": [_I],
-    "ndg_backward_mma": [_I, _L, _I, _P, _P, _P, _P, _P, _L, _P, _P],
+    "ndg_backward_mma": [_I, _L, _I, _P, _P, _P, _P, _P, _L, _L, _P, _P, _P],
     "ndg_active_mask": [_I, _L, _I, _P, _P, _P, _P, _L, _D, _P, _P, _P],
+    "ndg_backward_f64": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P, _P],
     "ndg_loss_f64": [_I, _I, _I, _I, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P],
     "ndg_epilogue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "ndg_adam": [_I, _L, _P, _P, _P, _P, _P, _I, _F, _F, _F, _F, _F, _F, _F, _P],
@@ -94,8 +96,8 @@ class NdgLaunchError(RuntimeError):
 
 # entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
 LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_scan_counts",
-             "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_backward", "ndg_backward_tc", "ndg_backward_mma",
-             "ndg_moments_to_zspace", "ndg_active_mask", "ndg_centre_records", "ndg_loss_f64", "ndg_epilogue", "ndg_adam",
+             "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_loss_rel_l2", "ndg_backward", "ndg_backward_mma",
+             "ndg_work_items", "ndg_bwd_bounds", "ndg_acc_dequant", "ndg_active_mask", "ndg_centre_records", "ndg_loss_f64", "ndg_backward_f64", "ndg_epilogue", "ndg_adam",
              "ndg_fp32_probe", "ndg_tf32_probe", "ndg_hmma_probe"}
 launch_count = 0
 

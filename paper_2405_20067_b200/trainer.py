@@ -135,8 +135,10 @@ class Trainer:
                  allreduce=None, rank: int = 0, world: int = 1):
         self.cfg, self.target, self.n = cfg, target, n_dims
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        # the sampling generator is seeded identically on every rank: each draws the same global batch
+        # and keeps its own tiles (datasets.sample_batch), so the ranks' tiles partition the 1-GPU batch
         self.gen = torch.Generator(device=self.device)
-        self.gen.manual_seed(cfg.seed * 1000003 + rank)
+        self.gen.manual_seed(cfg.seed * 1000003)
         self.rng = np.random.default_rng(cfg.seed)
         self.allreduce, self.rank, self.world = allreduce, rank, world
         if mixture is None:
@@ -150,6 +152,7 @@ class Trainer:
         self.state = new_adam_state(self.mix)
         self.low_count = torch.zeros(self.mix.G, dtype=torch.int32, device=self.device)
         self.step_no = 0
+        self.last_allreduce_bytes = 0
         self.last_good = self.mix.clone()
 
     def _init_gen(self):
@@ -161,9 +164,10 @@ class Trainer:
     def iteration(self) -> MetricsRow:
         cfg = self.cfg
         t0 = time.perf_counter()
-        q, tg = D.sample_batch(self.target, self.n, cfg.batch_size, cfg.tile_size, self.gen, self.device)
-        res = self.hp.fwd_bwd(self.mix, q, tg, cull=cfg.cull, n_total=cfg.batch_size * self.world,
-                              allreduce=self.allreduce)
+        q, tg = D.sample_batch(self.target, self.n, cfg.batch_size, cfg.tile_size, self.gen, self.device,
+                               self.rank, self.world)
+        res = self.hp.fwd_bwd(self.mix, q, tg, cull=cfg.cull, n_total=cfg.batch_size, allreduce=self.allreduce)
+        self.last_allreduce_bytes = res.grads.reduced().numel() * 4 if self.allreduce is not None else 0
         if not math.isfinite(res.loss):
             self.mix = self.last_good.clone()
             raise TrainingAborted(f"non-finite loss at iteration {self.step_no}", iteration=self.step_no)
@@ -178,6 +182,19 @@ class Trainer:
         self.low_count = torch.where(low, self.low_count + 1, torch.zeros_like(self.low_count))
         ms = (time.perf_counter() - t0) * 1e3
         return MetricsRow(self.step_no, res.loss, int(self.live_components()), 1.0 - res.kept_fraction, ms)
+
+    # -- resume state (resume is bit-identical) ----------------------------
+    def rng_state(self) -> dict:
+        """Everything random that the future of the fit depends on: the torch sampling generator
+        (identical on every rank) and the full numpy PCG64 state of the spawn RNG."""
+        return dict(seed=self.cfg.seed, torch=[int(b) for b in self.gen.get_state().tolist()],
+                    numpy=self.rng.bit_generator.state)
+
+    def set_rng_state(self, st: dict):
+        if "torch" in st:
+            self.gen.set_state(torch.tensor(st["torch"], dtype=torch.uint8))
+        if isinstance(st.get("numpy"), dict):
+            self.rng.bit_generator.state = st["numpy"]
 
     def live_components(self) -> int:
         return int(self.mix.G - int(((self.mix.flags & FLAG_FROZEN) != 0).sum()))

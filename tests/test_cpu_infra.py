@@ -60,10 +60,8 @@ def test_abi_layout_queries():
         rs = lib.ndg_record_floats(n)
         assert rs % 4 == 0 and rs >= 2 * n + n * (n - 1) // 2 + 3
         assert lib.ndg_query_floats(n) % 4 == 0 and lib.ndg_query_floats(n) >= n + 4
-        # S'[P] | t'[N] | spare (the moments' constant term) | gA[3] | stats[3]
+        # S'[P] | t'[N] | non-finite flag | gA[3] | stats[3]
         assert lib.ndg_accum_doubles(n) == O.n_chol(n) + n + 7
-        # tensor-core backward: moments of (N+1)(N+2)/2 features must fit one M=128 GEMM and smem
-        assert lib.ndg_backward_tc_supported(n) == (1 if n <= 12 else 0)
         # warp-MMA backward: one m16 block of dims, only where the FP32 K7's registers run short
         assert lib.ndg_backward_mma_supported(n) == (1 if 9 <= n <= 16 else 0)
     assert not lib.ndg_supported_dims(0) and not lib.ndg_supported_dims(17)

@@ -72,9 +72,12 @@ def test_bench_cull_ablation(cuda, tmp_path):
 
 
 def test_gradcheck_command(cuda):
-    """cmd_gradcheck: passes on random mixtures with live children across N and both
-    amplitude modes (reduced count here; the full default run takes ~8 s), and the negative control
-    (a corrupted analytic coordinate) fails."""
+    """cmd_gradcheck: the default run enforces SPEC.md:572's per-coordinate rule
+    (1e-4 relative, 1e-6 absolute floor) on the analytic chain rule fed by the float64 pair loop;
+    --fp32 checks the float32 product kernels under the relaxed block-relative rule. Reduced mixture
+    count here; the negative control (a corrupted analytic coordinate) fails both."""
     from paper_2405_20067_b200 import cli, gradcheck
     assert cli.main(["gradcheck", "--seed", "3", "--per-n", "4"]) == 0
+    assert cli.main(["gradcheck", "--seed", "3", "--per-n", "2", "--fp32"]) == 0
     assert not gradcheck.run(seed=3, per_n=1, dims=(4,), corrupt=True, out=lambda *_: None)
+    assert not gradcheck.run(seed=3, per_n=1, dims=(4,), corrupt=True, out=lambda *_: None, analytic="fp32")

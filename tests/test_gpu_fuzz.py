@@ -24,11 +24,11 @@ def _cases(n_cases=int(os.environ.get("NDG_FUZZ_CASES", "24")), seed=int(os.envi
         T = int(rng.integers(1, 5))
         G = int(rng.integers(1, 400))
         fwd = str(rng.choice(["tc", "fp32"]))
-        bwds = (["tc"] if N <= 12 else []) + ["fp32"] + (["mma"] if N >= 9 else [])
+        bwds = ["fp32"] + (["mma"] if N >= 9 else [])
         bwd = str(rng.choice(bwds))
         out.append(dict(N=N, tile=tile, B=tile * T, G=G, children=bool(rng.integers(0, 2)),
                         amp_mode=int(rng.integers(0, 2)), regime=str(rng.choice(["R", "C"])), fwd=fwd, bwd=bwd,
-                        sigma0=0.3 if bwd == "tc" else None, seed=int(rng.integers(0, 1000))))
+                        sigma0=None, seed=int(rng.integers(0, 1000))))
     return out
 
 

@@ -1,5 +1,5 @@
 """A/B of two K7 implementations on one workload: block-relative gradient differences between
-backward=<--other> ("mma" or "tc") and backward="fp32" (same forward), plus K7 timings.
+backward=<--other> ("mma") and backward="fp32" (same forward), plus K7 timings.
 Tuning aid, not a test."""
 import argparse, json, os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -16,7 +16,7 @@ ap.add_argument("--batch", type=int, default=1 << 16)
 ap.add_argument("--regime", default="R")
 ap.add_argument("--sigma0", type=float, default=None)
 ap.add_argument("--iters", type=int, default=2)
-ap.add_argument("--other", choices=["mma", "tc"], default="tc")
+ap.add_argument("--other", choices=["mma"], default="mma")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 kw = {} if a.sigma0 is None else dict(sigma0=a.sigma0)
