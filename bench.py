@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--regime", choices=["R", "C"], default="R")
+    ap.add_argument("--regime", choices=["R", "C", "G"], default="R")
     ap.add_argument("--n-dims", type=int, default=10)
     ap.add_argument("--gaussians", type=int, default=100_000)
     ap.add_argument("--batch", type=int, default=1 << 20, help="queries per GPU per step")
@@ -67,7 +67,7 @@ def workload_name(a, regime):
     return (f"{config_label(a)}: {a.n_dims}-D synthetic shading-shaped mixture, {a.gaussians} Gaussians"
             f"{' (+live children)' if a.children else ''}, {a.batch} queries/GPU/step, tile {a.tile}, "
             f"k={a.k}, multiplier 3, regime {regime} "
-            f"({'U[0,1)^N sorted by dim 0' if regime == 'R' else 'coherent tiles, spread 0.01'})")
+            f"({ {'R': 'U[0,1)^N sorted by dim 0', 'C': 'coherent tiles, spread 0.01', 'G': 'G-buffer-like: 2-D manifold, 16x16-pixel tiles, mixture seeded on the manifold, sigma0 0.005'}[regime] })")
 
 
 # ------------------------------------------------------------------------------------------------
@@ -293,7 +293,10 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
     import numpy as np
 
     from paper_2405_20067_b200 import parallel as P
-    mix_np, s0 = D.synthetic_mixture(a.n_dims, a.gaussians, seed=0, children=a.children)
+    if regime == "G":
+        mix_np, s0 = D.gbuffer_mixture(a.n_dims, a.gaussians, seed=0), 0.005
+    else:
+        mix_np, s0 = D.synthetic_mixture(a.n_dims, a.gaussians, seed=0, children=a.children)
     # one global batch of a.batch * world queries; rank r keeps global tiles r, r + world, ... (weak
     # scaling: a.batch queries per GPU)
     q = D.synthetic_queries(a.n_dims, a.batch * world, seed=1, regime=regime, tile_size=a.tile)
@@ -351,6 +354,8 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
     clk = clocks.stop() if clocks else None
     fwd_ms = statistics.mean(hp.kernel_ms("forward"))
     bwd_ms = statistics.mean(hp.kernel_ms("backward"))
+    cull_ms = statistics.mean(hp.kernel_ms("cull"))
+    plan = hp.prefilter_plan()
     hp.enable_kernel_timing(False)
     total_ms = sum(step_ms)
     if world > 1:
@@ -359,8 +364,23 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
         total_ms = float(tt)
     out = dict(total_ms=total_ms, ms_per_step=total_ms / steps, value=a.batch * world * steps / (total_ms * 1e-3),
                kept=statistics.mean(kept), pairs=statistics.mean(pairs), fwd_ms=fwd_ms, bwd_ms=bwd_ms,
+               cull_ms=cull_ms, prefilter_ran=bool(plan and plan[1]),
                launches=launches, clocks=clk, loss=res.loss, sigma0=s0, fwd_impl=hp.last_forward_impl,
                bwd_impl=hp.last_backward_impl)
+
+    # K4 alone, dense pass vs bucket pre-filter (same tile and projected bounds; identical masks)
+    recs = hp.activate(mix)
+    tb, pb = hp.tile_bounds(qd), hp.project(recs)
+    ab = {}
+    for mode in ("off", "on"):
+        hk = ndg.HotPath(a.n_dims, k=a.k, multiplier=3.0, tile_size=a.tile, projection_seed=2, device=dev,
+                         prefilter=mode)
+        hk.enable_kernel_timing(True)
+        for _ in range(3 + 10):
+            hk.cull(tb, pb)
+        torch.cuda.synchronize()
+        ab["dense" if mode == "off" else "prefilter"] = statistics.median(hk.kernel_ms("cull")[3:])
+    out["cull_ab"] = ab
 
     if measure_e2e:
         qh = torch.from_numpy(q).pin_memory()
@@ -408,13 +428,17 @@ def our_arm(a, rank, world):
                                          not a.no_e2e)
     secondary = None
     if not a.no_secondary:
-        other = "C" if a.regime == "R" else "R"
-        s, _ = run_regime(a, other, torch, ndg, D, K, dist, rank, world, dev, max(3, a.steps // 2), 3, False)
-        secondary = {f"regime_{other}": dict(value=s["value"], unit="queries/s", ms_per_step=s["ms_per_step"],
-                                             kept_fraction=s["kept"], pairs_per_step=s["pairs"],
-                                             workload=workload_name(a, other),
-                                             fp32_frac_step=s["pairs"] * ndg.kept_pairs_flops(a.n_dims)
-                                             / (s["ms_per_step"] * 1e-3) / 1e12 / peak)}
+        secondary = {}
+        for other in [r for r in ("R", "C", "G") if r != a.regime]:
+            s, _ = run_regime(a, other, torch, ndg, D, K, dist, rank, world, dev, max(3, a.steps // 2), 3, False)
+            secondary[f"regime_{other}"] = dict(
+                value=s["value"], unit="queries/s", ms_per_step=s["ms_per_step"], kept_fraction=s["kept"],
+                pairs_per_step=s["pairs"], workload=workload_name(a, other),
+                kernels_ms=dict(cull=s["cull_ms"], forward=s["fwd_ms"], backward=s["bwd_ms"]),
+                cull_impl="bucket pre-filter (K4p)" if s["prefilter_ran"] else "dense (K4a)",
+                fp32_frac_step=s["pairs"] * ndg.kept_pairs_flops(a.n_dims) / (s["ms_per_step"] * 1e-3) / 1e12 / peak)
+            if "cull_ab" in s:
+                secondary[f"regime_{other}"]["cull_ab_ms"] = s["cull_ab"]
     if rank != 0:
         if dist:
             dist.barrier()
@@ -430,6 +454,9 @@ def our_arm(a, rank, world):
     for v in kern.values():
         v["frac_of_measured_fp32"] = v["tflops"] / peak
         v["share_of_step"] = v["ms"] / main["ms_per_step"]
+    kern_cull = dict(ms=main["cull_ms"], share_of_step=main["cull_ms"] / main["ms_per_step"],
+                     impl="bucket pre-filter (K4p)" if main["prefilter_ran"] else "dense (K4a)",
+                     ab_ms=main["cull_ab"])
     if main["fwd_impl"] == "tc":
         # tensor-core forward: 3xTF32 z-GEMM, 3 * 2 * (N+1) * N algorithmic tensor flops per pair
         tc_f = 3 * 2 * (n + 1) * n
@@ -487,7 +514,7 @@ def our_arm(a, rank, world):
                       peak_nominal=NOMINAL_FP32_TFLOPS, frac_of_nominal=kern[dom]["tflops"] / NOMINAL_FP32_TFLOPS,
                       flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n)),
                       step_achieved=step_tflops, step_frac=step_tflops / peak)),
-        kernels=kern, gpu_launches=main["launches"], clocks=main["clocks"], loss=main["loss"],
+        kernels=dict(kern, cull=kern_cull), gpu_launches=main["launches"], clocks=main["clocks"], loss=main["loss"],
     )
     if "e2e" in main:
         line["e2e"] = main["e2e"]

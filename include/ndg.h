@@ -94,9 +94,20 @@ int ndg_tile_bounds(int n, int64_t B, int tile, const float* queries, const doub
                     double* hi, void* stream);
 
 /* K4a binning, phase 1. cull_tile for every tile: bit-mask [T][ceil(Gev/32)]
- * of kept candidates (warp ballot) and counts[T] (must be zeroed by the caller). */
+ * of kept candidates (warp ballot) and counts[T] (must be zeroed by the caller). 1 <= k <= 256. */
 int ndg_cull_mask(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* m_r,
                   const double* thr, uint32_t* mask, int64_t* counts, void* stream);
+
+/* K4a with a bucket pre-filter (the north_star's hash bucketing): live Gaussians
+ * are bucketed on a 64 x 64 grid over their projections on vectors 0 and 1; a tile runs the exact K4a
+ * test only on the Gaussians of the cells its intervals can reach, so the mask and counts are
+ * bit-identical to ndg_cull_mask's. A device-side plan (summed-area table of the cell populations)
+ * picks the pre-filtered or the dense pass per call (mode 0; 1 forces the pre-filter, 2 the dense
+ * pass); the other pass's kernels exit at once. workspace: ndg_cull_prefilter_workspace(Gev, k)
+ * bytes, no initialisation needed; counts zeroed by the caller; 2 <= k <= 256. */
+int64_t ndg_cull_prefilter_workspace(int64_t Gev, int k);
+int ndg_cull_prefilter(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* m_r,
+                       const double* thr, int mode, void* workspace, uint32_t* mask, int64_t* counts, void* stream);
 
 /* K4b exclusive scan of counts -> offsets[T+1] and backward work-item offsets[T+1]
  * (ceil(count / ndg_backward_chunk()) per tile). */
@@ -142,7 +153,7 @@ int ndg_forward_tc(int n, int64_t B, int tile, const float* queries, const float
  * loss_partial[ceil(B/256)] float64 block partials of mean((p - t)^2 / (p^2 + eps)) over 3 * n_total
  * entries, and dpred[B][3] (may be NULL) with the denominator detached; sum the partials
  * with ndg_loss_finalize. */
-int ndg_loss_rel_l2(int64_t B, const float* pred, const float* target, float eps, int64_t n_total, float* dpred,
+int ndg_loss_rel_l2(int64_t B, const float* pred, const float* target, double eps, int64_t n_total, float* dpred,
                     double* loss_partial, void* stream);
 
 /* Deterministic fixed-order sum of the per-tile loss partials. */
@@ -211,6 +222,27 @@ int ndg_active_mask(int n, int64_t B, int tile, const float* queries, const doub
 int ndg_loss_f64(int n, int G, int amp_mode, int M, const double* params, const double* child, const uint8_t* flags,
                  int64_t B, const float* queries, const float* targets, const double* inv_den, double* pred_out,
                  double* loss, void* stream);
+
+/*
+ * Error path of NonFiniteGradientError (the error names component, block and batch index):
+ * out[0] (int64, set to INT64_MAX by the caller) receives the lowest query index b of the step whose pair
+ * with evaluated Gaussian e1 or e2 (-1 = none), on a tile where it is a candidate in `mask`, gives a
+ * non-finite backward term in K7's float32 arithmetic (qrec / rec as passed to ndg_backward).
+ */
+int ndg_nonfinite_query(int n, int64_t B, int tile, const float* qrec, const float* rec, const uint32_t* mask,
+                        int64_t Gev, int64_t e1, int64_t e2, int64_t* out, void* stream);
+
+/*
+ * Diagnostic for cmd_gradcheck / finite_diff_grad: central finite differences of the
+ * rel-L2 loss in float64 (culling off, denominator held at pred_base: inv_den = 1 / (pred_base^2 + eps))
+ * for M raw coordinates coords[M][2] = (row, column), row < G a parent row, G <= row < 2G a child row;
+ * points = 2 ((l(+h) - l(-h)) / 2h) or 4 (the O(h^4) stencil). Only the Gaussians that read the
+ * perturbed row are re-evaluated, and the stencil is summed as sum_s w_s (2 d delta_s + delta_s^2)
+ * (d = pred_base - target, delta_s = their change), so the O(1) loss terms cancel exactly.
+ */
+int ndg_fd_f64(int n, int G, int amp_mode, const double* params, const double* child, const uint8_t* flags, int64_t B,
+               const float* queries, const float* targets, const double* pred_base, const double* inv_den, int M,
+               const int* coords, double h, int points, double* fd, void* stream);
 
 /*
  * Diagnostic for cmd_gradcheck: the backward pair loop in float64 (culling off, every query, one thread

@@ -113,8 +113,10 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
             // centred records hold (m_hi, m_lo) in the nb2 slots: z = rho ((x - m_hi) - m_lo), no cancellation
             float acc = CTR ? r[rec_rho(N) + i] * ((xq[i] - r[rec_nb2(N) + 2 * i]) - r[rec_nb2(N) + 2 * i + 1])
                             : fmaf(r[rec_rho(N) + i], xq[i], r[rec_nb2(N) + 2 * i]);
+#ifndef NDG_BWD_KO_SUBST   // knock-out build: drop the triangular solve's off-diagonal terms (wrong results)
 #pragma unroll
             for (int k = 0; k < i; ++k) acc = fmaf(r[rec_l(N, i, k)], (k & 1) ? z2[k / 2].y : z2[k / 2].x, acc);
+#endif
             if (i & 1) z2[i / 2].y = acc;
             else z2[i / 2].x = acc;
             s2 = fmaf(acc, acc, s2);
@@ -132,9 +134,11 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
 #pragma unroll
         for (int i = 0; i < N; ++i) {
             const float ui = (i & 1) ? u2[i / 2].y : u2[i / 2].x;
+#ifndef NDG_BWD_KO_S       // knock-out build: no S' update (wrong results)
 #pragma unroll
             for (int jp = 0; jp <= i / 2; ++jp)
                 Sp[srow_start(i) + jp] = __ffma2_rn(make_float2(ui, ui), z2[jp], Sp[srow_start(i) + jp]);
+#endif
         }
         gA0 = fmaf(g, dp0, gA0);
         gA1 = fmaf(g, dp1, gA1);

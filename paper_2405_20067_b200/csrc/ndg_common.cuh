@@ -86,9 +86,9 @@ constexpr double kC = 0.84932180028801907;      // sqrt(0.5 * log2(e))
 //   h-class (S', t', proxy): g z~_i z~_j <= max x 2^-x = 0.531, g |z~_i| and g sqrt(s~) <= 0.515, so
 //             |term| <= 0.54 |h| with |h| = |dpred . a| <= H * Amax;
 //   gA:       g |dpred_c| <= Dmax;     loss share: g ell <= Lmax;     pairs: exact integer counts.
-// H, Dmax, Lmax (over the step's queries) and Amax (over live Gaussians) come from ndg_bwd_bounds as
-// float bit patterns (uint32 atomicMax of non-negative floats; NaN sorts above +inf, so a non-finite
-// input poisons the scale and every partial is flagged).
+// H, Dmax, Lmax (over the step's finite queries) and Amax (over live Gaussians) come from
+// ndg_bwd_bounds as float bit patterns (uint32 atomicMax of non-negative floats); a non-finite query
+// makes only the partials it enters non-finite, and those set their Gaussian's flag.
 // ---------------------------------------------------------------------------------------------
 namespace ndg {
 

@@ -281,7 +281,8 @@ extern "C" int ndg_centre_records(int n, int64_t Gev, const double* mean64, cons
 // ---------------------------------------------------------------------------------------------
 // K4a cull mask: cull_tile for all tiles. Thread = evaluated Gaussian, CTA =
 // 256 Gaussians x TILES tiles; the tiles' intervals sit in shared memory and are broadcast, the
-// Gaussian's (m_r, thr) live in registers for k <= 16 (shared memory otherwise). Culled iff any
+// Gaussian's (m_r, thr) live in registers for k <= 16 (read through L1 for larger k, which keeps the
+// shared memory at 2 * 16 * k doubles for any k <= 256). Culled iff any
 // vector has lo - m_r > thr or m_r - hi > thr (FP64; the same predicate as
 // max(lo - m_r, m_r - hi, 0) > multiplier * s_r); thr < 0 = never evaluated. Warp ballot -> one mask
 // word per 32 Gaussians; per-CTA popcount -> one atomic per tile.
@@ -298,13 +299,13 @@ __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int 
                                                                   const double* __restrict__ m_r,
                                                                   const double* __restrict__ thr,
                                                                   uint32_t* __restrict__ mask,
-                                                                  int64_t* __restrict__ counts) {
+                                                                  int64_t* __restrict__ counts,
+                                                                  const unsigned long long* __restrict__ skip) {
     constexpr int TILES = REG ? kCullTilesReg : kCullTilesSmem;
+    if (skip && *skip) return;                     // the bucket pre-filter (ndg_cull_prefilter) took this step
     extern __shared__ double sm[];
     double* s_lo = sm;                             // [TILES][k]
     double* s_hi = s_lo + TILES * k;
-    double* s_m = s_hi + TILES * k;                // [k][256] (shared-memory path only)
-    double* s_t = s_m + k * kCullThreads;
     __shared__ int s_cnt[TILES][kCullThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t e = blockIdx.x * (int64_t)kCullThreads + tid;
@@ -324,10 +325,6 @@ __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int 
         }
         never = th_r[0] < 0.0;
     } else {
-        for (int ri = 0; ri < k; ++ri) {
-            s_m[ri * kCullThreads + tid] = e < Gev ? m_r[ri * Gev + e] : 0.0;
-            s_t[ri * kCullThreads + tid] = e < Gev ? thr[ri * Gev + e] : -1.0;
-        }
         never = (e < Gev ? thr[e] : -1.0) < 0.0;
     }
     __syncthreads();
@@ -354,8 +351,8 @@ __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int 
             }
 #endif
         } else {
-            for (int ri = 0; ri < k && kept; ++ri) {
-                const double mr = s_m[ri * kCullThreads + tid], th = s_t[ri * kCullThreads + tid];
+            for (int ri = 0; ri < k && kept; ++ri) {          // kept is false for e >= Gev (never)
+                const double mr = __ldg(m_r + ri * Gev + e), th = __ldg(thr + ri * Gev + e);
                 const double l = s_lo[tt * k + ri], h = s_hi[tt * k + ri];
                 if (__dsub_rn(l, mr) > th || __dsub_rn(mr, h) > th) kept = false;
             }
@@ -375,26 +372,32 @@ __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int 
     }
 }
 
-extern "C" int ndg_cull_mask(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* m_r,
-                             const double* thr, uint32_t* mask, int64_t* counts, void* stream) {
-    NDG_REQUIRE(k >= 1 && k <= 64, "k must be in 1..64 for the cull kernel");
+int cull_mask_launch(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* m_r,
+                     const double* thr, uint32_t* mask, int64_t* counts, const unsigned long long* skip,
+                     cudaStream_t stream) {
+    NDG_REQUIRE(k >= 1 && k <= 256, "k must be in 1..256 for the cull kernel");
     if (T == 0 || Gev == 0) return NDG_OK;
     const bool reg = k <= kCullRegK;
     const int tiles = reg ? kCullTilesReg : kCullTilesSmem;
     dim3 grid((unsigned)((Gev + kCullThreads - 1) / kCullThreads), (unsigned)((T + tiles - 1) / tiles));
     NDG_REQUIRE(grid.y <= 65535, "too many tiles for one cull launch");
-    const size_t smem = sizeof(double) * (2 * tiles * k + (reg ? 0 : 2 * k * kCullThreads));
+    const size_t smem = sizeof(double) * 2 * tiles * k;    // <= 64 KB at k = 256
     static DeviceOnce attr_set;
     if (attr_set.first()) {
         cudaFuncSetAttribute(cull_mask_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         cudaFuncSetAttribute(cull_mask_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     }
     if (reg)
-        cull_mask_kernel<true><<<grid, kCullThreads, smem, as_stream(stream)>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts);
+        cull_mask_kernel<true><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts, skip);
     else
-        cull_mask_kernel<false><<<grid, kCullThreads, smem, as_stream(stream)>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts);
+        cull_mask_kernel<false><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts, skip);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
+}
+
+extern "C" int ndg_cull_mask(int64_t T, int k, int64_t Gev, const double* lo, const double* hi, const double* m_r,
+                             const double* thr, uint32_t* mask, int64_t* counts, void* stream) {
+    return cull_mask_launch(T, k, Gev, lo, hi, m_r, thr, mask, counts, nullptr, as_stream(stream));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -506,6 +509,8 @@ extern "C" int ndg_work_items(int64_t T, const int64_t* chunk_offsets, int64_t* 
 // Dmax = max_q,c |dpred_c|, Lmax = max_q ell over the step's query records, Amax = max |a_c| over live
 // Gaussians -- as float bit patterns (uint32 atomicMax of non-negative values; `bounds` zeroed by the
 // caller). Order-independent, so the scales every K7 launch derives from them are deterministic.
+// Non-finite inputs are left out: the partials they enter are themselves non-finite and flag only
+// their own Gaussians (-> NonFiniteGradientError naming the component).
 // ---------------------------------------------------------------------------------------------
 __global__ void bwd_bounds_kernel(int n, int64_t B, const float* __restrict__ qrec, int64_t Gev,
                                   const float* __restrict__ rec, const uint8_t* __restrict__ eflags,
@@ -516,13 +521,15 @@ __global__ void bwd_bounds_kernel(int n, int64_t B, const float* __restrict__ qr
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < B; q += stride) {
         const float* r = qrec + q * QS + n;
         const float a0 = fabsf(r[0]), a1 = fabsf(r[1]), a2 = fabsf(r[2]);
-        h = max(h, __float_as_uint(fabsf(a0 + a1 + a2)));
+        if (!isfinite(a0 + a1 + a2 + r[3])) continue;   // a non-finite query flags only the pairs it enters
+        h = max(h, __float_as_uint(a0 + a1 + a2));
         d = max(d, max(__float_as_uint(a0), max(__float_as_uint(a1), __float_as_uint(a2))));
         l = max(l, __float_as_uint(fabsf(r[3])));
     }
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < Gev; e += stride) {
         if ((eflags[e] & 3) != 1) continue;       // live, not degenerate
         const float* r = rec + e * RS + A0;
+        if (!isfinite(r[0] + r[1] + r[2])) continue;
         am = max(am, max(__float_as_uint(fabsf(r[0])), max(__float_as_uint(fabsf(r[1])), __float_as_uint(fabsf(r[2])))));
     }
     h = __reduce_max_sync(0xffffffffu, h);
@@ -663,7 +670,7 @@ __global__ void loss_finalize_kernel(int64_t T, const double* __restrict__ part,
 // NULL) = 2 (p - t) / (p^2 + eps) / (3 n_total), the gradient with the denominator detached (:291).
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) loss_rel_l2_kernel(int64_t B, const float* __restrict__ pred,
-                                                          const float* __restrict__ target, float eps, int64_t n_total,
+                                                          const float* __restrict__ target, double eps, int64_t n_total,
                                                           float* __restrict__ dpred, double* __restrict__ part) {
     __shared__ double s[256];
     const int64_t b = blockIdx.x * 256LL + threadIdx.x;
@@ -671,7 +678,7 @@ __global__ void __launch_bounds__(256) loss_rel_l2_kernel(int64_t B, const float
     if (b < B) {
         const double inv = 1.0 / (3.0 * (double)n_total);
         for (int c = 0; c < 3; ++c) {
-            const double p = pred[b * 3 + c], d = p - (double)target[b * 3 + c], den = p * p + (double)eps;
+            const double p = pred[b * 3 + c], d = p - (double)target[b * 3 + c], den = p * p + eps;
             l += d * d / den;
             if (dpred) dpred[b * 3 + c] = (float)(2.0 * d / den * inv);
         }
@@ -686,9 +693,9 @@ __global__ void __launch_bounds__(256) loss_rel_l2_kernel(int64_t B, const float
     if (threadIdx.x == 0) part[blockIdx.x] = s[0];
 }
 
-extern "C" int ndg_loss_rel_l2(int64_t B, const float* pred, const float* target, float eps, int64_t n_total,
+extern "C" int ndg_loss_rel_l2(int64_t B, const float* pred, const float* target, double eps, int64_t n_total,
                                float* dpred, double* loss_partial, void* stream) {
-    NDG_REQUIRE(eps > 0.f && n_total >= 1, "eps > 0 and n_total >= 1 required (SPEC.md:255)");
+    NDG_REQUIRE(eps > 0.0 && n_total >= 1, "eps > 0 and n_total >= 1 required (SPEC.md:255)");
     if (B == 0) return NDG_OK;
     loss_rel_l2_kernel<<<(unsigned)((B + 255) / 256), 256, 0, as_stream(stream)>>>(B, pred, target, eps, n_total,
                                                                                     dpred, loss_partial);

@@ -79,7 +79,8 @@ def sort_into_tiles(q: np.ndarray, targets: np.ndarray | None = None):
 
 def synthetic_queries(n: int, B: int, seed: int = 1, *, regime: str = "R", tile_size: int = 256,
                       spread: float = 0.01) -> np.ndarray:
-    """R: U[0,1)^N sorted by dim 0 (the reference sampler); C: coherent tiles (centre + N(0, spread^2))."""
+    """R: U[0,1)^N sorted by dim 0 (the reference sampler); C: coherent tiles (centre + N(0, spread^2));
+    G: G-buffer-like queries on a 2-D manifold (gbuffer_queries)."""
     rng = np.random.default_rng(seed)
     if regime == "R":
         q = rng.random((B, n))
@@ -88,10 +89,66 @@ def synthetic_queries(n: int, B: int, seed: int = 1, *, regime: str = "R", tile_
         T = B // tile_size
         centre = rng.random((T, 1, n))
         q = np.clip(centre + rng.normal(0.0, spread, (T, tile_size, n)), 0.0, 1.0).reshape(B, n)
+    elif regime == "G":
+        return gbuffer_queries(n, B, seed, tile_size)
     else:
         raise ValueError(f"unknown regime {regime!r}")
     return q.astype(np.float32)
 
+
+def gbuffer_queries(n: int, B: int, seed: int = 1, tile_size: int = 256):
+    """Regime G: G-buffer-like queries on a 2-D manifold in N-D. Pixels of a
+    W x H image (W = 2^ceil(log2(B)/2)), grouped into square tiles of tile_size pixels (16 x 16 at 256):
+    position (u, v, height(u, v)) | view direction to a fixed camera (mapped to [0,1]) | albedo(u, v) |
+    roughness(u, v) | further smooth "variable" dims for N > 10; the first N features, float32. Tiles
+    are tight in every dimension, so culling keeps only a few tens of Gaussians per tile and the
+    binning (K4), not the pair loops, dominates the step."""
+    rng = np.random.default_rng(seed)
+    ph = rng.uniform(0.0, 1.0, 16)
+    W = 1 << int(math.ceil(math.log2(max(B, 1)) / 2))
+    H = B // W
+    ts = int(round(math.sqrt(tile_size)))
+    if ts * ts != tile_size or W % ts or H % ts or W * H != B:
+        raise ValueError("regime G needs B = W * H with square tiles dividing the image")
+    ty, tx, j, i = np.meshgrid(np.arange(H // ts), np.arange(W // ts), np.arange(ts), np.arange(ts), indexing="ij")
+    px, py = (tx * ts + i).reshape(-1), (ty * ts + j).reshape(-1)
+    u, v = (px + 0.5) / W, (py + 0.5) / H
+    tau = 2.0 * np.pi
+    h = 0.5 + 0.2 * np.sin(tau * (1.3 * u + ph[0])) * np.cos(tau * (0.9 * v + ph[1])) + 0.1 * np.sin(tau * (3.1 * u + 2.7 * v))
+    cam = np.array([0.5, -0.8, 1.6])
+    d = cam[None, :] - np.stack([u, v, h], 1)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    feats = [u, v, h, 0.5 * (d[:, 0] + 1), 0.5 * (d[:, 1] + 1), 0.5 * (d[:, 2] + 1)]
+    for c in range(3):
+        feats.append(0.5 + 0.4 * np.sin(tau * (2.0 * u + ph[2 + c])) * np.cos(tau * (1.5 * v + ph[5 + c])))
+    feats.append(0.5 + 0.45 * np.sin(tau * (u + v + ph[8])))
+    k = 0
+    while len(feats) < n:
+        k += 1
+        feats.append(0.5 + 0.4 * np.sin(tau * (k * u + (k + 1) * v + ph[9 + k % 7])))
+    return np.stack(feats[:n], 1).astype(np.float32)
+
+
+def gbuffer_mixture(n: int, G: int, seed: int = 0, *, sigma0: float = 0.005, amp_mode: int = BRIGHTNESS):
+    """Mixture for regime G: means at the manifold features of G random pixels of a 1024 x 1024 image
+    (gbuffer_queries' geometry), diagonal raw ln(sigma0) + U[-1/2, 1/2], off-diagonal raw N(0, sigma0^2),
+    colour N(0, 1), amplitude as synthetic_mixture. Float32 rows."""
+    rng = np.random.default_rng(seed)
+    feats = gbuffer_queries(n, 1 << 20, seed=1)
+    ms, cs, cols, amp = raw_slices(n)
+    R = raw_width(n)
+    params = np.zeros((G, R))
+    params[:, ms] = feats[rng.integers(0, feats.shape[0], G)]
+    for i in range(n):
+        for j in range(i + 1):
+            if i == j:
+                params[:, cs.start + tri(i, j)] = math.log(sigma0) + rng.uniform(-0.5, 0.5, G)
+            else:
+                params[:, cs.start + tri(i, j)] = rng.normal(0.0, sigma0, G)
+    params[:, cols] = rng.normal(0.0, 1.0, (G, 3))
+    params[:, amp] = rng.normal(math.log(0.1) if amp_mode == BRIGHTNESS else -2.0, 0.5, G)
+    return dict(params=params.astype(np.float32), child=np.zeros((G, R), np.float32), has_child=np.zeros(G, bool),
+                frozen=np.zeros(G, bool))
 
 def synthetic_targets(B: int, seed: int = 3) -> np.ndarray:
     return np.random.default_rng(seed).random((B, 3)).astype(np.float32)

@@ -195,8 +195,10 @@ def decode_status(st, G: int, n: int) -> int:
             if cls is InvalidParameterError:
                 raise InvalidParameterError(f"non-finite raw parameter ({which} row, block {_BLOCKS[blk]})",
                                             component=int(comp), block=_BLOCKS[blk], entry=int(entry))
-            raise NonFiniteGradientError(f"non-finite gradient ({which} row, block {_BLOCKS[blk]})",
+            err = NonFiniteGradientError(f"non-finite gradient ({which} row, block {_BLOCKS[blk]})",
                                          component=int(comp), block=_BLOCKS[blk], batch_index=-1)
+            err.child_row = which == "child"
+            raise err
     return int(st[2])
 
 
@@ -205,7 +207,7 @@ class HotPath:
 
     def __init__(self, n_dims: int, *, k: int = 16, multiplier: float = 3.0, tile_size: int = 256,
                  eps: float = 0.01, projection_seed: int = 0, projections: ProjectionSet | None = None,
-                 device=None, forward: str | None = None, backward: str | None = None):
+                 device=None, forward: str | None = None, backward: str | None = None, prefilter: str | None = None):
         self.n = int(n_dims)
         self.L = K.layout(self.n)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -233,6 +235,13 @@ class HotPath:
         if bwd == "mma" and not (lib.ndg_backward_mma_supported(self.n) and self.tile % 8 == 0):
             bwd = "fp32"
         self.backward_impl = bwd
+        # K4 binning: "auto" = bucket pre-filter when the device-side plan finds it cheaper (tight tiles,
+        # narrow Gaussians), else the dense pass; "on" forces the pre-filter, "off" the plain dense kernel.
+        # All three give bit-identical candidate lists.
+        self.prefilter = prefilter or os.environ.get("NDG_PREFILTER", "auto")
+        if self.prefilter not in ("auto", "on", "off"):
+            raise ValueError("prefilter must be 'auto', 'on' or 'off'")
+        self._pf_ws = None
         self._recs = None    # the last activation: its conditioning bound rides on the cull's read-back
         self.last_forward_impl = self.last_backward_impl = None   # what the last step ran
         self.last_centred = False
@@ -240,7 +249,7 @@ class HotPath:
 
     def enable_kernel_timing(self, on: bool = True):
         """Record CUDA events on the launching stream around the K5 and K7 launches."""
-        self.events = {"forward": [], "backward": []} if on else None
+        self.events = {"forward": [], "backward": [], "cull": []} if on else None
 
     def _ev(self, name, when):
         if self.events is None:
@@ -253,7 +262,8 @@ class HotPath:
             self.events[name][-1][1] = e
 
     def kernel_ms(self, name):
-        """Per-launch durations (ms) of the recorded launches of K5 ("forward") / K7 ("backward")."""
+        """Per-launch durations (ms) of the recorded launches of K5 ("forward"), K7 ("backward") and the
+        K4a / K4p cull mask ("cull")."""
         return [a.elapsed_time(b) for a, b in self.events[name]]
 
     # -- K1 --------------------------------------------------------------------------------
@@ -353,9 +363,25 @@ class HotPath:
         W = (Gev + 31) // 32
         mask = torch.empty(T, W, dtype=torch.int32, device=self.device)
         counts = torch.zeros(T, dtype=torch.int64, device=self.device)
-        K.call("ndg_cull_mask", T, k, Gev, _p(tb.lo), _p(tb.hi), _p(pb.m_r), _p(pb.thr), _p(mask), _p(counts),
-               _stream())
+        self._ev("cull", 0)
+        if self.prefilter != "off" and k >= 2:
+            nb = int(K.load().ndg_cull_prefilter_workspace(Gev, k))
+            if self._pf_ws is None or self._pf_ws.numel() < nb:
+                self._pf_ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
+            K.call("ndg_cull_prefilter", T, k, Gev, _p(tb.lo), _p(tb.hi), _p(pb.m_r), _p(pb.thr),
+                   1 if self.prefilter == "on" else 0, _p(self._pf_ws), _p(mask), _p(counts), _stream())
+        else:
+            K.call("ndg_cull_mask", T, k, Gev, _p(tb.lo), _p(tb.hi), _p(pb.m_r), _p(pb.thr), _p(mask), _p(counts),
+                   _stream())
+        self._ev("cull", 1)
         return self._finish_lists(T, Gev, counts, mask)
+
+    def prefilter_plan(self):
+        """(tests the pre-filtered pass counted, 1 if it ran) for the last cull, from the device plan."""
+        if self._pf_ws is None:
+            return None
+        st = self._pf_ws[:64].view(torch.int64).cpu().tolist()
+        return int(st[6]), int(st[7])
 
     def all_active(self, T: int, recs: EvalRecords) -> CandidateLists:
         """Culling disabled (SPEC.md:276 finite differences, SPEC.md:562 --no-cull): every live
@@ -463,6 +489,24 @@ class HotPath:
                _p(self.status), _stream())
         return accum
 
+    def nonfinite_batch_index(self, mix: Mixture, recs: EvalRecords, cl: CandidateLists, qrec, err) -> int:
+        """Error path of NonFiniteGradientError: the lowest index into this call's query
+        batch at which the offending component's pairs (its own Gaussian, and for a parent row also its
+        live child, whose composition reads the parent) give a non-finite backward term; -1 when no pair
+        does (the non-finite value arose in the epilogue's solve)."""
+        if cl.mask is None or qrec is None:
+            return -1
+        G, i = mix.G, int(err.component)
+        if getattr(err, "child_row", False):
+            e1, e2 = G + i, -1
+        else:
+            e1, e2 = i, (G + i if recs.Gev == 2 * G else -1)
+        out = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=self.device)
+        K.call("ndg_nonfinite_query", self.n, int(qrec.shape[0]), self.tile, _p(qrec), _p(recs.rec), _p(cl.mask),
+               recs.Gev, e1, e2, _p(out), _stream())
+        b = int(out.cpu()[0])
+        return -1 if b == _INT64_MAX else b
+
     # -- status ----------------------------------------------------------------------------
     def reset_status(self):
         self.status.zero_()
@@ -504,12 +548,24 @@ class HotPath:
         if allreduce is not None:
             allreduce(grads.reduced())
         host = torch.cat([self.status, loss.view(torch.int64)]).cpu()
-        n_deg = self.check_status(mix, host[:4]) if check else 0
+        try:
+            n_deg = self.check_status(mix, host[:4]) if check else 0
+        except NonFiniteGradientError as err:
+            err.batch_index = self.nonfinite_batch_index(mix, recs, cl, qrec, err)
+            raise
         loss_v = float(host[4:5].view(torch.float64)[0]) if allreduce is None else float(grads.scalars[0])
         return StepResult(loss_v, pred, grads, cl, n_deg, cl.kept_fraction(recs.Gev))
 
     def evaluate(self, mix: Mixture, queries, *, cull: bool = True) -> torch.Tensor:
-        """Culled evaluation at every query (cmd_eval's path)."""
+        """Culled evaluation at every query (cmd_eval's path). A batch that is not a
+        multiple of the tile size is padded with copies of its last query and the result sliced."""
+        B = int(queries.shape[0])
+        pad = (-B) % self.tile
+        if pad:
+            if B == 0:
+                return torch.zeros(0, 3, dtype=torch.float32, device=self.device)
+            return self.evaluate(mix, torch.cat([queries, queries[-1:].expand(pad, queries.shape[1])]).contiguous(),
+                                 cull=cull)[:B]
         self.reset_status()
         recs = self.activate(mix)
         T = int(queries.shape[0]) // self.tile

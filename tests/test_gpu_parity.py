@@ -366,17 +366,19 @@ def test_loss_f64_evaluator_vs_oracle(cuda, N, amp_mode):
     assert abs(float(loss.cpu()[0]) - ref["loss"]) <= 1e-12 * abs(ref["loss"])
 
 
-@pytest.mark.parametrize("shrink", [1.5, 40.0])
+@pytest.mark.parametrize("shrink", [1.5, 10.0, 400.0])
 def test_sharp_outliers_among_broad(cuda, shrink):
     """A few Gaussians `shrink` x sharper than the rest: the conditioning guard looks at the worst
     single Gaussian (HotPath.TC_FORWARD_PEAK_BOUND), not only the RMS, so the outliers' OWN gradient
     rows stay within 1e-4 (row-relative) as well as every block."""
     ndg = _ndg()
-    om, _ = O.synthetic_mixture(10, 600, seed=3, sigma0=0.15)
-    sharp = np.arange(0, 600, 75)                      # 8 outliers
+    om, _ = O.synthetic_mixture(10, 3000, seed=3, sigma0=0.15)
+    sharp = np.arange(0, 3000, 375)                    # 8 outliers among 3000
     ms, cs, cols, amp = O.raw_slices(10)
     for i in range(10):
         om.params[sharp, cs.start + O.tri(i, i)] -= np.log(shrink)
+        for j in range(i):        # off-diagonal activations are not scale-relative (SPEC.md:131): keep them 0
+            om.params[sharp, cs.start + O.tri(i, j)] = 0.0
     q = O.synthetic_queries(10, 2048, seed=4, regime="C")
     q[:256 * len(sharp)] = np.clip(om.params[np.repeat(sharp, 256), :10] +
                                    np.random.default_rng(5).normal(0, 0.15 / shrink, (256 * len(sharp), 10)), 0, 1)
@@ -387,7 +389,7 @@ def test_sharp_outliers_among_broad(cuda, shrink):
     recs = hp.activate(mix)
     assert recs.tc_conditioning() <= hp.TC_FORWARD_MAX_BOUND          # the RMS alone would allow TC
     assert (hp.last_forward_impl == "tc") == (recs.tc_peak() <= hp.TC_FORWARD_PEAK_BOUND)
-    if shrink > 10:
+    if shrink > 100:
         assert hp.last_forward_impl == "fp32" and hp.last_centred
     ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
     got = res.grads.params.cpu().numpy()
@@ -397,3 +399,76 @@ def test_sharp_outliers_among_broad(cuda, shrink):
         if nr > 1e-6 * np.linalg.norm(ref["grad_parent"]):
             e = np.linalg.norm(got[r] - ref["grad_parent"][r]) / nr
             assert e < RTOL, f"outlier row {r}: {e:.3e}"
+
+
+@pytest.mark.parametrize("k", [37, 64, 200])
+def test_cull_many_projection_vectors(cuda, k):
+    """k past the register path (k > 16) up to 256: the cull reads (m_r, thr) through L1 and keeps its
+    shared memory bounded; candidate lists stay bit-exact."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(6, 700, 2048, regime="C")
+    hp = ndg.HotPath(6, k=k, projection_seed=4)
+    cl = hp.cull(hp.tile_bounds(torch.from_numpy(q).cuda()), hp.project(hp.activate(mix)))
+    ev = O.build_eval_set(om)
+    mr, sr, thr = O.project_components(ev, hp.ps.vectors, 3.0)
+    lo, hi = O.tile_bounds(q, hp.ps.vectors, 256)
+    off, idx = O.cull_csr(lo, hi, mr, thr)
+    assert np.array_equal(cl.offsets.cpu().numpy(), off) and np.array_equal(cl.idx.cpu().numpy(), idx)
+
+
+def test_nonfinite_gradient_names_component_block_and_batch_index(cuda):
+    """SPEC.md:267 / errors.py:26-33: a non-finite target at query 300 makes the backward non-finite;
+    the error names the lowest offending component, its block, and the batch index 300."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(4, 64, 1024, regime="R")
+    t = t.copy()
+    t[300, 1] = np.nan
+    hp = ndg.HotPath(4, projection_seed=2)
+    with pytest.raises(ndg.NonFiniteGradientError) as ei:
+        hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
+    e = ei.value
+    assert e.block in ("mean", "chol", "color", "amp") and 0 <= e.component < 64
+    assert e.batch_index == 300
+
+
+@pytest.mark.parametrize("N,G,B,regime,children,k", [
+    (10, 3000, 16384, "G", False, 16),
+    (10, 2000, 16384, "G", True, 16),
+    (6, 1500, 4096, "C", True, 16),
+    (10, 1200, 4096, "R", False, 16),
+    (4, 800, 4096, "G", False, 2),
+    (8, 900, 4096, "C", False, 40),
+])
+def test_prefilter_candidate_lists_bit_identical(cuda, N, G, B, regime, children, k):
+    """The bucket pre-filter (ndg_cull_prefilter) forced on, left to the device plan, and off all give
+    the oracle's candidate lists bit for bit; in the G-buffer-like regime the plan takes the
+    pre-filter, with uniform queries (R) it keeps the dense pass."""
+    ndg = _ndg()
+    from paper_2405_20067_b200 import datasets as D
+    if regime == "G":
+        om = O.gbuffer_mixture(N, G, seed=3)
+        if children:
+            om2, _ = O.synthetic_mixture(N, G, seed=3, children=True)
+            om.child, om.has_child = om2.child, om2.has_child
+    else:
+        om, _ = O.synthetic_mixture(N, G, seed=3, children=children)
+    q = D.synthetic_queries(N, B, seed=4, regime=regime)
+    mix = ndg.Mixture.from_arrays(N, 0, om.params, om.child, om.has_child, om.frozen)
+    qd = torch.from_numpy(q).cuda()
+    ev = O.build_eval_set(om)
+    R = O.make_projection_set(N, k, 2)
+    mr, sr, thr = O.project_components(ev, R, 3.0)
+    lo, hi = O.tile_bounds(q, R, 256)
+    off, idx = O.cull_csr(lo, hi, mr, thr)
+    plans = {}
+    for mode in ("on", "auto", "off"):
+        hp = ndg.HotPath(N, k=k, projection_seed=2, prefilter=mode)
+        cl = hp.cull(hp.tile_bounds(qd), hp.project(hp.activate(mix)))
+        assert np.array_equal(cl.offsets.cpu().numpy(), off), mode
+        assert np.array_equal(cl.idx.cpu().numpy(), idx), mode
+        plans[mode] = hp.prefilter_plan()
+    assert plans["on"][1] == 1 and plans["off"] is None
+    if regime == "G" and k == 16:
+        assert plans["auto"][1] == 1
+    if regime == "R":
+        assert plans["auto"][1] == 0

@@ -96,3 +96,20 @@ def test_no_spike_shading_toy(cuda):
     assert spikes[0][0] < 0.01                                          # pure spawn event
     clean = [sp for sp, ev in spikes if ev["clamped"] == 0]
     assert clean and max(clean) < 0.01, spikes
+
+
+def test_gmm_target_any_batch_and_component_count(cuda):
+    """HotPath.evaluate pads batches that are not a tile multiple (gmm fits with
+    n_components = 300 or tile 128 / batch 384 no longer crash), and the padded result equals the
+    unpadded evaluation of the same queries."""
+    D, T = _T()
+    tgt = D.GmmOracleTarget(0, 4, 6)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1)
+    q = torch.rand(300, 4, generator=g, device="cuda")
+    p300 = tgt(q)
+    p512 = tgt(torch.cat([q, q[:212]]))
+    assert p300.shape == (300, 3) and torch.equal(p300, p512[:300])
+    cfg = T.TrainConfig(iterations=3, n_components=300, batch_size=384, tile_size=128)
+    res = T.train(cfg, tgt, 4)
+    assert len(res.metrics) == 3 and all(np.isfinite(r.loss) for r in res.metrics)

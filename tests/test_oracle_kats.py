@@ -175,7 +175,7 @@ def test_cull_conservative_randomized():
     """zero culled components with density >= exp(-4.5) at a tile query."""
     rng = np.random.default_rng(7)
     viol = 0
-    for trial in range(200):
+    for trial in range(1000):                         # SPEC.md:573: 1000 randomized instances
         n = int(rng.integers(2, 11))
         om, _ = O.synthetic_mixture(n, 60, seed=trial, sigma0=float(rng.uniform(0.03, 0.2)))
         ev = O.build_eval_set(om)
@@ -326,10 +326,15 @@ def test_adam_kats():
     p2, m1, m2 = O.adam_step(p, np.zeros(4), np.zeros(4), np.zeros(4), 1, 1e-2)
     assert np.array_equal(p2, p)
     m1 = m2 = np.zeros(1)
-    x = np.zeros(1, np.float32)
+    x = np.zeros(1, np.float64)
+    steps = []
     for s in range(1, 200):
+        x_prev = x.copy()
         x, m1, m2 = O.adam_step(x, np.full(1, 0.5), m1, m2, s, 1e-2)
-    assert (x[0] - (-0.01 * 198)) == pytest.approx(x[0] + 1.98, abs=1e-3) and x[0] < -1.9
+        steps.append(float(x[0] - x_prev[0]))
+    # under a constant gradient the bias-corrected step tends to -lr * sign(g)
+    assert abs(steps[-1] + 0.01) < 1e-6 and abs(steps[0] + 0.01) < 1e-6
+    assert abs(float(x[0]) + 0.01 * 199) < 1e-4
     x = np.array([3.0], np.float32)
     m1 = m2 = np.zeros(1)
     for s in range(1, 501):
