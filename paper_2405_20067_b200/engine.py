@@ -357,6 +357,10 @@ class HotPath:
         return TileBounds(lo, hi, self.tile)
 
     # -- K4 --------------------------------------------------------------------------------
+    # The pre-filter's device plan costs a handful of small launches: below this many (tile, Gaussian)
+    # tests the dense pass is cheaper than deciding (cfg1: 64 tiles x 4096 Gaussians = 2.6e5).
+    PREFILTER_MIN_TESTS = 1 << 22
+
     def cull(self, tb: TileBounds, pb: ProjectedBounds) -> CandidateLists:
         T, k = int(tb.lo.shape[0]), int(tb.lo.shape[1])
         Gev = int(pb.m_r.shape[1])
@@ -364,7 +368,9 @@ class HotPath:
         mask = torch.empty(T, W, dtype=torch.int32, device=self.device)
         counts = torch.zeros(T, dtype=torch.int64, device=self.device)
         self._ev("cull", 0)
-        if self.prefilter != "off" and k >= 2:
+        self._pf_used = k >= 2 and (self.prefilter == "on" or
+                                    (self.prefilter == "auto" and T * Gev >= self.PREFILTER_MIN_TESTS))
+        if self._pf_used:
             nb = int(K.load().ndg_cull_prefilter_workspace(Gev, k))
             if self._pf_ws is None or self._pf_ws.numel() < nb:
                 self._pf_ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
@@ -378,7 +384,7 @@ class HotPath:
 
     def prefilter_plan(self):
         """(tests the pre-filtered pass counted, 1 if it ran) for the last cull, from the device plan."""
-        if self._pf_ws is None:
+        if self._pf_ws is None or not getattr(self, "_pf_used", False):
             return None
         st = self._pf_ws[:64].view(torch.int64).cpu().tolist()
         return int(st[6]), int(st[7])

@@ -28,7 +28,8 @@ def _cases(n_cases=int(os.environ.get("NDG_FUZZ_CASES", "24")), seed=int(os.envi
         bwd = str(rng.choice(bwds))
         out.append(dict(N=N, tile=tile, B=tile * T, G=G, children=bool(rng.integers(0, 2)),
                         amp_mode=int(rng.integers(0, 2)), regime=str(rng.choice(["R", "C"])), fwd=fwd, bwd=bwd,
-                        sigma0=None, seed=int(rng.integers(0, 1000))))
+                        sigma0=None, seed=int(rng.integers(0, 1000)),
+                        prefilter=str(rng.choice(["auto", "on", "off"]))))
     return out
 
 
@@ -40,7 +41,7 @@ def _rel(a, b, floor=1e-30):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), floor))
 
 
-@pytest.mark.parametrize("case", _cases(), ids=lambda c: "N{N}-t{tile}-B{B}-G{G}-{fwd}-{bwd}".format(**c))
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: "N{N}-t{tile}-B{B}-G{G}-{fwd}-{bwd}-pf{prefilter}".format(**c))
 def test_fuzz_fwd_bwd(cuda, case):
     import paper_2405_20067_b200 as ndg
     c = case
@@ -49,7 +50,8 @@ def test_fuzz_fwd_bwd(cuda, case):
     q = O.synthetic_queries(c["N"], c["B"], seed=c["seed"] + 1, regime=c["regime"], tile_size=c["tile"])
     t = O.synthetic_targets(c["B"], seed=c["seed"] + 3)
     mix = ndg.Mixture.from_arrays(c["N"], c["amp_mode"], om.params, om.child, om.has_child, om.frozen)
-    hp = ndg.HotPath(c["N"], tile_size=c["tile"], projection_seed=c["seed"] + 2, forward=c["fwd"], backward=c["bwd"])
+    hp = ndg.HotPath(c["N"], tile_size=c["tile"], projection_seed=c["seed"] + 2, forward=c["fwd"], backward=c["bwd"],
+                     prefilter=c["prefilter"])
     res = hp.fwd_bwd(mix, torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda())
     ref = O.fwd_bwd(om, q, t, hp.ps.vectors, tile_size=c["tile"])
     assert np.array_equal(res.candidates.offsets.cpu().numpy(), ref["offsets"])
