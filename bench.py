@@ -365,6 +365,7 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
     out = dict(total_ms=total_ms, ms_per_step=total_ms / steps, value=a.batch * world * steps / (total_ms * 1e-3),
                kept=statistics.mean(kept), pairs=statistics.mean(pairs), fwd_ms=fwd_ms, bwd_ms=bwd_ms,
                cull_ms=cull_ms, prefilter_ran=bool(plan and plan[1]),
+               allreduce_bytes=int(grads.reduced().numel()) * 4,
                launches=launches, clocks=clk, loss=res.loss, sigma0=s0, fwd_impl=hp.last_forward_impl,
                bwd_impl=hp.last_backward_impl)
 
@@ -497,6 +498,7 @@ def our_arm(a, rank, world):
                     evaluated_gaussians=a.gaussians * (2 if a.children else 1), batch_per_gpu=a.batch,
                     global_batch=a.batch * world, tile=a.tile, k=a.k, multiplier=3.0, regime=a.regime,
                     kept_fraction=main["kept"], pairs_per_step=pairs, sigma0=main["sigma0"],
+                    allreduce_payload_bytes_per_step=main["allreduce_bytes"],
                     l2="flushed before every timed step (256 MiB write, outside the timed interval)",
                     parallelism=f"dp{world} (one global batch of {a.batch * world} queries, strided tiles per "
                                 f"rank, mixture replicated, 1 {(dist.get_backend() if dist else 'nccl').upper()} "

@@ -26,6 +26,7 @@ under the relaxed block-relative 1e-4 rule, and says so in its output.
 from __future__ import annotations
 
 import argparse
+import json
 import math
 import os
 import sys
@@ -141,7 +142,10 @@ def cmd_fit(args) -> int:
                       file=sys.stderr)
             if (it + 1) % cfg.phase_length == 0:
                 if (it + 1) // cfg.phase_length >= cfg.warmup_phases:
-                    tr.phase_event()
+                    ev = tr.phase_event()
+                    if rank == 0:       # refinement events with the phase's density statistics
+                        with open(os.path.join(args.out, "events.jsonl"), "a") as fe:
+                            fe.write(json.dumps(ev, sort_keys=True) + "\n")
                     if world > 1 and rank == 0:
                         print(f"phase event at {it + 1}: {tr.mix.G} components, children live "
                               f"{tr.mix.children_live}", file=sys.stderr)

@@ -45,6 +45,23 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+class _NvtxRange:
+    """NVTX range around one stage when NDG_NVTX=1 (for nsys / ncu --nvtx); free otherwise."""
+    on = os.environ.get("NDG_NVTX", "0") == "1"
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if self.on:
+            torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *exc):
+        if self.on:
+            torch.cuda.nvtx.range_pop()
+        return False
+
+
 # ----------------------------------------------------------------------------------------------
 # culling types (SPEC.md:152-175)
 # ----------------------------------------------------------------------------------------------
@@ -530,7 +547,8 @@ class HotPath:
         collective) before the status / loss read-back. `candidates` -- when given --
         are the per-tile active sets to use (SPEC.md:263's "active sets per tile"), e.g. from cull()."""
         self.reset_status()
-        recs = self.activate(mix)
+        with _NvtxRange("ndg.K1 activate"):
+            recs = self.activate(mix)
         T = int(queries.shape[0]) // self.tile
         if candidates is not None:
             if candidates.T != T:
@@ -538,21 +556,25 @@ class HotPath:
             cl = candidates
             recs.tc_conditioning()                       # the read-back cull() would have carried
         elif cull:
-            pb = self.project(recs)
-            tb = self.tile_bounds(queries)
-            cl = self.cull(tb, pb)
+            with _NvtxRange("ndg.K2-K4 bounds + cull"):
+                pb = self.project(recs)
+                tb = self.tile_bounds(queries)
+                cl = self.cull(tb, pb)
         else:
             cl = self.all_active(T, recs)
-        pred, qrec, loss_part = self.forward(queries, recs, cl, targets, n_total)
-        loss = self.finalize_loss(loss_part)
+        with _NvtxRange("ndg.K5 forward + loss"):
+            pred, qrec, loss_part = self.forward(queries, recs, cl, targets, n_total)
+            loss = self.finalize_loss(loss_part)
         if grads is None:
             grads = alloc_gradients(mix.G, recs.Gev, self.n, self.device)
-        self.backward(mix, recs, cl, qrec, grads)
+        with _NvtxRange("ndg.K7-K8 backward"):
+            self.backward(mix, recs, cl, qrec, grads)
         grads.scalars[0] = loss[0].to(torch.float32)
         grads.scalars[1] = float(cl.n_pairs_tiles * self.tile)
         grads.children_live = recs.Gev == 2 * mix.G
         if allreduce is not None:
-            allreduce(grads.reduced())
+            with _NvtxRange("ndg.allreduce"):
+                allreduce(grads.reduced())
         host = torch.cat([self.status, loss.view(torch.int64)]).cpu()
         try:
             n_deg = self.check_status(mix, host[:4]) if check else 0

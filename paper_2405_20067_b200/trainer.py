@@ -153,6 +153,7 @@ class Trainer:
         self.low_count = torch.zeros(self.mix.G, dtype=torch.int32, device=self.device)
         self.step_no = 0
         self.last_allreduce_bytes = 0
+        self.phase_stats = None       # [Gev, 3] float64 on the device: the phase's density statistics
         self.last_good = self.mix.clone()
 
     def _init_gen(self):
@@ -172,6 +173,10 @@ class Trainer:
             self.mix = self.last_good.clone()
             raise TrainingAborted(f"non-finite loss at iteration {self.step_no}", iteration=self.step_no)
         self.step_no += 1
+        st = res.grads.stats.double()
+        if self.phase_stats is None or self.phase_stats.shape != st.shape:
+            self.phase_stats = torch.zeros_like(st)
+        self.phase_stats += st
         adam_step(self.mix, res.grads, self.state, self.step_no,
                   lr=(cfg.lr_mean, cfg.lr_chol, cfg.lr_color, cfg.lr_amp), betas=(cfg.beta1, cfg.beta2),
                   eps=cfg.adam_eps)
@@ -200,11 +205,31 @@ class Trainer:
         return int(self.mix.G - int(((self.mix.flags & FLAG_FROZEN) != 0).sum()))
 
     # -- refinement events ---------------------------------------------
+    def density_summary(self) -> dict:
+        """The phase's density-control statistics (north_star; gathered inside K7, summed over the
+        phase's iterations on the device): totals, the components no tile query reached (zero pairs)
+        and the components carrying the largest loss share. Reported with every refinement event."""
+        if self.phase_stats is None:
+            return {}
+        ps = self.phase_stats.cpu().numpy()
+        G = self.mix.G
+        parent = ps[:G]
+        out = dict(loss_share=float(ps[:, 0].sum()), grad_proxy=float(ps[:, 1].sum()), pairs=float(ps[:, 2].sum()),
+                   unreached_components=int(np.count_nonzero(parent[:, 2] == 0)),
+                   top_loss_share=[int(i) for i in np.argsort(-parent[:, 0], kind="stable")[:8]])
+        if ps.shape[0] == 2 * G:
+            out["child_loss_share"] = float(ps[G:, 0].sum())
+        return out
+
     def phase_event(self):
-        """One refinement boundary: freeze-out, check_materialize + materialize, spawn_children."""
+        """One refinement boundary: freeze-out, check_materialize + materialize, spawn_children. The
+        event record carries the phase's density statistics (density_summary)."""
+        stats = self.density_summary()
+        self.phase_stats = None
         ev = self.materialize_step()
         ev["spawned"] = self.spawn_step()
         ev["n_components"] = self.mix.G
+        ev["density_stats"] = stats
         self.last_good = self.mix.clone()
         return ev
 

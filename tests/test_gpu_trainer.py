@@ -113,3 +113,18 @@ def test_gmm_target_any_batch_and_component_count(cuda):
     cfg = T.TrainConfig(iterations=3, n_components=300, batch_size=384, tile_size=128)
     res = T.train(cfg, tgt, 4)
     assert len(res.metrics) == 3 and all(np.isfinite(r.loss) for r in res.metrics)
+
+
+def test_phase_events_carry_density_statistics(cuda):
+    """The density-control statistics gathered inside K7 are summed over each phase and reported with
+    the refinement event (north_star)."""
+    D, T = _T()
+    tgt = D.GmmOracleTarget(3, 4, 6)
+    cfg = T.TrainConfig(iterations=60, phase_length=30, warmup_phases=1, n_components=48, batch_size=2048, seed=4)
+    res = T.train(cfg, tgt, 4)
+    assert len(res.events) == 2
+    for ev in res.events:
+        ds = ev["density_stats"]
+        assert ds["loss_share"] > 0 and ds["grad_proxy"] > 0 and ds["pairs"] > 0
+        assert 0 <= ds["unreached_components"] <= ev["n_components"] and len(ds["top_loss_share"]) == 8
+    assert "child_loss_share" in res.events[1]["density_stats"]          # children live in phase 2
