@@ -256,7 +256,10 @@ def cmd_bench_cull(args) -> int:
     mults = [float(x) for x in aslist(b.get("multiplier_list"), [1, 2, 3, 4])]
     tiles = [int(x) for x in aslist(b.get("tile_list"), [64, 256])]
     dev = torch.device("cuda", torch.cuda.current_device())
-    mix_np, _ = D.synthetic_mixture(n, G, seed=seed, sigma0=b.get("sigma0"))
+    if regime == "G":      # G-buffer-like inference workload: mixture seeded on the query manifold
+        mix_np = D.gbuffer_mixture(n, G, seed=seed, sigma0=float(b.get("sigma0", 0.005)))
+    else:
+        mix_np, _ = D.synthetic_mixture(n, G, seed=seed, sigma0=b.get("sigma0"))
     mix = Mixture.from_arrays(n, 0, **mix_np, device=dev)
     qd = torch.from_numpy(D.synthetic_queries(n, B, seed=seed + 1, regime=regime)).to(dev)
 
