@@ -231,6 +231,8 @@ def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, generator
     q = q[order]
     if world > 1:
         T = batch_size // tile_size
+        if T < world:
+            raise ValueError(f"{T} tiles cannot give each of {world} ranks one (batch_size / tile_size >= world)")
         q = q.view(T, tile_size, n_dims)[rank::world].reshape(-1, n_dims)
     q = q.contiguous()
     return q, target(q).contiguous()

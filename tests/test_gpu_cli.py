@@ -19,6 +19,11 @@ def test_fit_eval_resume(cuda, tmp_path):
     assert rows[0] == "iteration,loss,n_components,culled_fraction,ms_per_iter" and len(rows) == 41
     ck = F.load_checkpoint(out / "checkpoint.ndgc")
     assert ck["iteration"] == 40 and ck["params"].shape[0] >= 64
+    # refinement events at iterations 20 and 40, each with the phase's density statistics
+    import json
+    evs = [json.loads(x) for x in (out / "events.jsonl").read_text().splitlines()]
+    assert [e["iteration"] for e in evs] == [20, 40] and evs[0]["spawned"] > 0
+    assert all(e["density_stats"]["pairs"] > 0 for e in evs)
     # resume for 20 more iterations
     cfgp.write_text(cfgp.read_text().replace("iterations = 40", "iterations = 60"))
     out2 = tmp_path / "run2"
