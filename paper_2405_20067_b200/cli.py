@@ -50,14 +50,15 @@ def _target(cfg: dict, n_dims: int, device):
 
 
 def _state_of(tr, cfg_raw):
-    m = tr.mix
+    m = tr.full_mixture()            # the ordered mixture: frozen rows (compacted out of the loop) in place
+    st, low = tr.full_state()
     return dict(n_dims=m.n_dims, amp_mode=m.amp_mode, iteration=tr.step_no, adam_step=tr.step_no,
                 config=cfg_raw, dataset=cfg_raw.get("data", {}),
                 rng=tr.rng_state(),
                 params=m.params.cpu().numpy(), child=m.child.cpu().numpy(), flags=m.flags.cpu().numpy(),
-                m1p=tr.state["m1p"].cpu().numpy(), m2p=tr.state["m2p"].cpu().numpy(),
-                m1c=tr.state["m1c"].cpu().numpy(), m2c=tr.state["m2c"].cpu().numpy(),
-                low_count=tr.low_count.cpu().numpy())
+                m1p=st["m1p"].cpu().numpy(), m2p=st["m2p"].cpu().numpy(),
+                m1c=st["m1c"].cpu().numpy(), m2c=st["m2c"].cpu().numpy(),
+                low_count=low.cpu().numpy())
 
 
 def _dist_setup():
@@ -112,11 +113,7 @@ def cmd_fit(args) -> int:
                                   (fl & FLAG_FROZEN) != 0, device=dev)
     tr = Trainer(cfg, target, n, mixture=mix, device=dev, allreduce=allreduce, rank=rank, world=world)
     if st is not None:
-        tr.step_no = int(st["iteration"])
-        for k in ("m1p", "m2p", "m1c", "m2c"):
-            tr.state[k] = torch.from_numpy(st[k]).to(dev)
-        tr.low_count = torch.from_numpy(st["low_count"]).to(dev)
-        tr.set_rng_state(st.get("rng", {}))
+        tr.resume(st)
     metrics = None
     if rank == 0:
         path = os.path.join(args.out, "metrics.csv")

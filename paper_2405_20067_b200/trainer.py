@@ -2,11 +2,18 @@
 
 One iteration: sample batch → tile → cull → forward → loss → backward → Adam, i.e. one
 `HotPath.fwd_bwd` (K1-K8, plus the single NCCL all_reduce when data-parallel) and one `adam_step`
-(K9) on the device. Refinement events run between iterations on the host ("single
-threaded between iterations") every `phase_length` iterations after `warmup_phases` phases:
-check_materialize → materialize → spawn_children, and components whose activated
-amplitude stayed below t/100 for a whole phase are frozen out. New rows and children
-start with zeroed Adam moments.
+(K9) on the device. Refinement events run between iterations ("single threaded between
+iterations") every `phase_length` iterations after `warmup_phases` phases, on the device (tensor ops
+on the SoA rows; the composed child factors come from K1): check_materialize → materialize →
+spawn_children, and components whose activated amplitude stayed below t/100 for a
+whole phase are frozen out. New rows and children start with zeroed Adam moments
+(SPEC.md:322).
+
+Frozen components are compacted out of the working set: their rows move to an archive and the K1-K8
+passes, Adam and the allreduce only see live rows. Every row keeps an id (its position in the
+reference's ordered mixture: original rows first, materialized rows appended in event order), and
+`full_mixture()` / `full_state()` merge the archive back in id order for checkpoints and results, so
+the saved mixture is the one the uncompacted loop would hold (frozen rows in place, flagged).
 """
 from __future__ import annotations
 
@@ -18,7 +25,7 @@ import numpy as np
 import torch
 
 from . import datasets as D
-from .engine import HotPath, adam_step, alloc_gradients, new_adam_state
+from .engine import HotPath, adam_step, new_adam_state
 from .errors import TrainingAborted
 from .gmm import BRIGHTNESS, FLAG_CHILD, FLAG_FROZEN, Mixture, n_chol, raw_slices, raw_width, tri
 
@@ -85,26 +92,6 @@ def _activate(chol_raw, n):
     return L
 
 
-def _inverse_activate(L, n, clamp=1.0 - 1e-6):
-    raw = np.zeros(L.shape[:-2] + (n_chol(n),))
-    clamped = 0
-    for i in range(n):
-        for j in range(i + 1):
-            v = L[..., i, j]
-            if i == j:
-                raw[..., tri(i, j)] = np.log(v)
-            else:
-                vc = np.clip(v, -clamp, clamp)          # clamp to +-(1 - 1e-6) and log it
-                clamped += int(np.count_nonzero(vc != v))
-                s = (vc + 1.0) / 2.0
-                raw[..., tri(i, j)] = np.log(s) - np.log1p(-s)
-    return raw, clamped
-
-
-def _amp(raw, mode):
-    return np.exp(raw) if mode == BRIGHTNESS else _sigmoid(raw)
-
-
 def spawn_rows(n, count, mode, t, rng):
     """spawn_children: U = I, m_u = 0, color_raw in +-0.1, activated amp = t/10."""
     ms, cs, cols, amp = raw_slices(n)
@@ -147,6 +134,9 @@ class Trainer:
             mixture = initial_mixture(cfg, n_dims, q0[torch.randperm(q0.shape[0], generator=self._init_gen(),
                                                                      device=self.device)], self.device)
         self.mix = mixture
+        self.ids = torch.arange(self.mix.G, dtype=torch.int64, device=self.device)
+        self.next_id = self.mix.G
+        self.archive = None           # frozen rows compacted out of the working set (params, child, flags, ids)
         self.hp = HotPath(n_dims, k=cfg.k, multiplier=cfg.multiplier, tile_size=cfg.tile_size, eps=cfg.loss_eps,
                           projection_seed=cfg.seed, device=self.device)
         self.state = new_adam_state(self.mix)
@@ -202,7 +192,7 @@ class Trainer:
             self.rng.bit_generator.state = st["numpy"]
 
     def live_components(self) -> int:
-        return int(self.mix.G - int(((self.mix.flags & FLAG_FROZEN) != 0).sum()))
+        return int(self.mix.G - int(((self.mix.flags & FLAG_FROZEN) != 0).sum()))   # frozen rows are archived
 
     # -- refinement events ---------------------------------------------
     def density_summary(self) -> dict:
@@ -228,69 +218,138 @@ class Trainer:
         self.phase_stats = None
         ev = self.materialize_step()
         ev["spawned"] = self.spawn_step()
-        ev["n_components"] = self.mix.G
+        ev["n_components"] = self.mix.G + (0 if self.archive is None else int(self.archive["ids"].numel()))
+        ev["live_components"] = self.mix.G
         ev["density_stats"] = stats
         self.last_good = self.mix.clone()
         return ev
 
-    def _host(self):
-        mix = self.mix
-        return (mix.params.double().cpu().numpy(), mix.child.double().cpu().numpy(), mix.flags.cpu().numpy().copy(),
-                {k: v.cpu().numpy() for k, v in self.state.items()})
+    # -- working set <-> the reference's ordered mixture ---------------------------------------------
+    def _compact(self):
+        """Move frozen rows (out of optimisation and evaluation) to the archive."""
+        fr = (self.mix.flags & FLAG_FROZEN) != 0
+        if not bool(fr.any()):
+            return 0
+        keep = ~fr
+        moved = dict(params=self.mix.params[fr], child=self.mix.child[fr], flags=self.mix.flags[fr], ids=self.ids[fr])
+        self.archive = moved if self.archive is None else {k: torch.cat([self.archive[k], moved[k]])
+                                                            for k in moved}
+        fl = self.mix.flags[keep].contiguous()
+        self.mix = Mixture(self.n, self.cfg.amp_mode, self.mix.params[keep].contiguous(),
+                           self.mix.child[keep].contiguous(), fl, bool(((fl & FLAG_CHILD) != 0).any()))
+        self.state = {k: v[keep].contiguous() for k, v in self.state.items()}
+        self.low_count = self.low_count[keep].contiguous()
+        self.ids = self.ids[keep].contiguous()
+        return int(fr.sum())
 
-    def _upload(self, params, child, has_child, frozen, st):
-        self.mix = Mixture.from_arrays(self.n, self.cfg.amp_mode, params.astype(np.float32), child.astype(np.float32),
-                                       has_child, frozen, device=self.device)
-        self.state = {k: torch.from_numpy(np.ascontiguousarray(v)).to(self.device) for k, v in st.items()}
-        if self.low_count.shape[0] != self.mix.G:
-            self.low_count = torch.cat([self.low_count, torch.zeros(self.mix.G - self.low_count.shape[0],
-                                                                    dtype=torch.int32, device=self.device)])
+    def _merged(self, active: dict, archived: dict):
+        if self.archive is None:
+            return active
+        order = torch.argsort(torch.cat([self.ids, self.archive["ids"]]))
+        return {k: torch.cat([active[k], archived[k]])[order].contiguous() for k in active}
+
+    def full_mixture(self) -> Mixture:
+        """The whole ordered mixture: live rows and the archived frozen rows (flagged), in id order."""
+        m = self._merged(dict(params=self.mix.params, child=self.mix.child, flags=self.mix.flags),
+                         self.archive or {})
+        fl = m["flags"]
+        return Mixture(self.n, self.cfg.amp_mode, m["params"], m["child"], fl,
+                       bool((((fl & FLAG_CHILD) != 0) & ((fl & FLAG_FROZEN) == 0)).any()))
+
+    def full_state(self):
+        """(Adam moments, low-amplitude counters) over the whole ordered mixture; archived rows: zeros."""
+        na = 0 if self.archive is None else int(self.archive["ids"].numel())
+        z = lambda v: torch.zeros((na,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)  # noqa: E731
+        st = self._merged(dict(self.state), {k: z(v) for k, v in self.state.items()})
+        lc = self._merged(dict(lc=self.low_count), dict(lc=z(self.low_count)))["lc"]
+        return st, lc
+
+    def resume(self, ckpt: dict):
+        """Continue from a checkpoint: iteration, Adam moments, freeze counters and RNG
+        state over the saved ordered mixture (this Trainer was built on it), then compact."""
+        self.step_no = int(ckpt["iteration"])
+        for k in ("m1p", "m2p", "m1c", "m2c"):
+            self.state[k] = torch.from_numpy(np.ascontiguousarray(ckpt[k])).to(self.device)
+        self.low_count = torch.from_numpy(np.ascontiguousarray(ckpt["low_count"])).to(self.device)
+        self.set_rng_state(ckpt.get("rng", {}))
+        self._compact()
+        self.last_good = self.mix.clone()
 
     def materialize_step(self):
         """Freeze-out, then check_materialize and materialize
-        (SPEC.md:356-364): each selected child becomes a standalone component (composed mean and
-        factor, activations inverted with off-diagonal clamping); its parent loses the child."""
+        (SPEC.md:356-364): each selected child becomes a standalone component with the composed mean
+        and factor (K1's float64 m_c = L m_u + m_p and L U), activations inverted with off-diagonal
+        clamping to +-(1 - 1e-6); its parent loses the child. All on the device."""
         cfg, n = self.cfg, self.n
         t = cfg.threshold()
-        params, child, flags, st = self._host()
         ms, cs, cols, amp = raw_slices(n)
+        mix = self.mix
+        G = mix.G
+        flags = mix.flags.clone()
+        newly_frozen = (self.low_count >= cfg.phase_length) & ((flags & FLAG_FROZEN) == 0)
+        flags = torch.where(newly_frozen, (flags | FLAG_FROZEN) & ~FLAG_CHILD, flags)
         has_child = (flags & FLAG_CHILD) != 0
-        frozen = (flags & FLAG_FROZEN) != 0
-        newly_frozen = (self.low_count.cpu().numpy() >= cfg.phase_length) & ~frozen
-        frozen |= newly_frozen
-        has_child &= ~frozen
-        idx = np.flatnonzero(has_child & (_amp(child[:, amp], cfg.amp_mode) >= t))
-        Lp = _activate(params[idx][:, cs], n)
-        U = _activate(child[idx][:, cs], n)
-        mc = np.einsum("eik,ek->ei", Lp, child[idx][:, ms]) + params[idx][:, ms]
-        new_rows = np.zeros((idx.size, raw_width(n)))
-        new_rows[:, ms] = mc
-        new_rows[:, cs], clamped = _inverse_activate(Lp @ U, n)
-        new_rows[:, cols] = child[idx][:, cols]
-        new_rows[:, amp] = child[idx][:, amp]
-        has_child[idx] = False
-        k = idx.size
-        zeros = np.zeros((k, raw_width(n)))
-        for key in st:                                  # new slots start with zero moments (SPEC.md:322)
-            st[key] = np.concatenate([st[key], zeros.astype(np.float32)])
-        self._upload(np.concatenate([params, new_rows]), np.concatenate([child, zeros]),
-                     np.concatenate([has_child, np.zeros(k, bool)]), np.concatenate([frozen, np.zeros(k, bool)]), st)
+        camp = mix.child[:, amp].double()
+        alpha = torch.exp(camp) if cfg.amp_mode == BRIGHTNESS else torch.sigmoid(camp)
+        sel = torch.nonzero(has_child & (alpha >= t)).flatten()
+        k = int(sel.numel())
+        clamped = 0
+        if k:
+            recs = self.hp.activate(mix)                 # composed child rows e = G + i, float64
+            e = G + sel
+            new_rows = torch.zeros(k, raw_width(n), dtype=torch.float64, device=self.device)
+            new_rows[:, ms] = recs.mean64[e]
+            L = recs.chol64[e]
+            raw = torch.empty_like(L)
+            lim = 1.0 - 1e-6
+            for i in range(n):
+                for j in range(i + 1):
+                    v = L[:, tri(i, j)]
+                    if i == j:
+                        raw[:, tri(i, j)] = torch.log(v)
+                    else:
+                        vc = v.clamp(-lim, lim)
+                        clamped += int((vc != v).sum())
+                        s_ = (vc + 1.0) / 2.0
+                        raw[:, tri(i, j)] = torch.log(s_) - torch.log1p(-s_)
+            new_rows[:, cs] = raw
+            new_rows[:, cols] = mix.child[sel][:, cols].double()
+            new_rows[:, amp] = mix.child[sel][:, amp].double()
+            flags[sel] = flags[sel] & ~FLAG_CHILD
+            zf = torch.zeros(k, raw_width(n), dtype=torch.float32, device=self.device)
+            params = torch.cat([mix.params, new_rows.float()])
+            child = torch.cat([mix.child, zf])
+            flags = torch.cat([flags, torch.zeros(k, dtype=torch.uint8, device=self.device)])
+            self.state = {key: torch.cat([v, zf]) for key, v in self.state.items()}   # zero moments (SPEC.md:322)
+            self.low_count = torch.cat([self.low_count, torch.zeros(k, dtype=torch.int32, device=self.device)])
+            self.ids = torch.cat([self.ids, torch.arange(self.next_id, self.next_id + k, dtype=torch.int64,
+                                                         device=self.device)])
+            self.next_id += k
+        else:
+            params, child = mix.params, mix.child
+        self.mix = Mixture(n, cfg.amp_mode, params.contiguous(), child.contiguous(), flags.contiguous(),
+                           bool((((flags & FLAG_CHILD) != 0) & ((flags & FLAG_FROZEN) == 0)).any()))
         self.low_count.zero_()
-        return dict(iteration=self.step_no, materialized=int(k), frozen=int(newly_frozen.sum()), clamped=int(clamped))
+        self._compact()
+        return dict(iteration=self.step_no, materialized=k, frozen=int(newly_frozen.sum()), clamped=int(clamped))
 
     def spawn_step(self) -> int:
         """spawn_children: every live component without a child gets one (U = I,
-        m_u = 0, colour in +-0.1 raw, activated amplitude t/10) with zeroed moments."""
+        m_u = 0, colour in +-0.1 raw from the checkpointed spawn RNG, activated amplitude t/10) with
+        zeroed moments."""
         cfg, n = self.cfg, self.n
-        params, child, flags, st = self._host()
-        has_child = (flags & FLAG_CHILD) != 0
-        frozen = (flags & FLAG_FROZEN) != 0
-        needs = ~has_child & ~frozen
-        child[needs] = spawn_rows(n, int(needs.sum()), cfg.amp_mode, cfg.threshold(), self.rng)
-        for key in ("m1c", "m2c"):
-            st[key][needs] = 0.0
-        self._upload(params, child, has_child | needs, frozen, st)
-        return int(needs.sum())
+        mix = self.mix
+        needs = ((mix.flags & FLAG_CHILD) == 0) & ((mix.flags & FLAG_FROZEN) == 0)
+        cnt = int(needs.sum())
+        if cnt:
+            rows = torch.from_numpy(spawn_rows(n, cnt, cfg.amp_mode, cfg.threshold(), self.rng)).to(self.device)
+            child = mix.child.clone()
+            child[needs] = rows
+            for key in ("m1c", "m2c"):
+                self.state[key][needs] = 0.0
+            flags = torch.where(needs, mix.flags | FLAG_CHILD, mix.flags)
+            self.mix = Mixture(n, cfg.amp_mode, mix.params, child, flags.contiguous(), True)
+        return cnt
 
 
 def train(cfg: TrainConfig, target, n_dims: int, *, mixture: Mixture | None = None, device=None, allreduce=None,
@@ -306,7 +365,7 @@ def train(cfg: TrainConfig, target, n_dims: int, *, mixture: Mixture | None = No
             callback(tr, row)
         if (it + 1) % cfg.phase_length == 0 and (it + 1) // cfg.phase_length >= cfg.warmup_phases:
             out.events.append(tr.phase_event())
-    out.mixture = tr.mix
+    out.mixture = tr.full_mixture()
     return out
 
 

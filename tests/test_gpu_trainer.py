@@ -128,3 +128,56 @@ def test_phase_events_carry_density_statistics(cuda):
         assert ds["loss_share"] > 0 and ds["grad_proxy"] > 0 and ds["pairs"] > 0
         assert 0 <= ds["unreached_components"] <= ev["n_components"] and len(ds["top_loss_share"]) == 8
     assert "child_loss_share" in res.events[1]["density_stats"]          # children live in phase 2
+
+
+def _dim_rows(tr, rows):
+    """Drop a few components' amplitude far below t/100 so the next event freezes them."""
+    p = tr.mix.params.clone()
+    p[rows, -1] = float(np.log(1e-7))
+    tr.mix.params = p
+
+
+def test_frozen_rows_are_compacted_and_checkpointed_in_place(cuda, tmp_path):
+    """Freeze-out moves frozen rows out of the working set (K1-K8, Adam, allreduce see
+    only live rows); full_mixture() restores them in place, flagged, and a fit resumed from the
+    checkpoint of such a state continues bitwise like the uninterrupted one."""
+    from paper_2405_20067_b200 import cli
+    from paper_2405_20067_b200 import formats as F
+    from paper_2405_20067_b200.gmm import FLAG_FROZEN, Mixture
+    D, T = _T()
+    tgt = D.GmmOracleTarget(5, 4, 6)
+    cfg = T.TrainConfig(iterations=80, phase_length=20, warmup_phases=1, n_components=64, batch_size=2048, seed=6)
+
+    def run(stop, resume_from=None):
+        if resume_from is None:
+            tr = T.Trainer(cfg, tgt, 4)
+            _dim_rows(tr, [3, 10, 20])
+        else:
+            ck = F.load_checkpoint(resume_from)
+            fl = ck["flags"]
+            mix = Mixture.from_arrays(4, ck["amp_mode"], ck["params"], ck["child"], (fl & 1) != 0, (fl & 2) != 0)
+            tr = T.Trainer(cfg, tgt, 4, mixture=mix)
+            tr.resume(ck)
+        while tr.step_no < stop:
+            tr.iteration()
+            if tr.step_no % cfg.phase_length == 0:
+                tr.phase_event()
+        path = tmp_path / f"ck_{stop}_{resume_from is not None}.ndgc"
+        F.save_checkpoint(path, cli._state_of(tr, {}))
+        return tr, path
+
+    full, pfull = run(80)
+    assert full.archive is not None and set(full.archive["ids"].tolist()) >= {3, 10, 20}
+    fm = full.full_mixture()
+    fl = fm.flags.cpu().numpy()
+    assert all(fl[i] & FLAG_FROZEN for i in (3, 10, 20))
+    assert fm.G == full.mix.G + full.archive["ids"].numel()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(2)
+    q, _ = D.sample_batch(tgt, 4, 2048, 256, g, "cuda")
+    a = full.hp.evaluate(full.mix, q, cull=False)
+    b = full.hp.evaluate(fm, q, cull=False)
+    assert torch.equal(a, b)                                   # frozen rows contribute nothing either way
+    half, phalf = run(40)
+    resumed, pres = run(80, resume_from=phalf)
+    assert pres.read_bytes() == pfull.read_bytes()
