@@ -1,5 +1,5 @@
 """Prints the z-GEMM conditioning bound max_e B_e (ndg_tc_records) of seeded synthetic mixtures, the
-quantity HotPath compares with TC_FORWARD_MAX_BOUND / TC_BACKWARD_MAX_BOUND. Tuning aid."""
+quantities HotPath compares with TC_FORWARD_MAX_BOUND (RMS) and TC_FORWARD_PEAK_BOUND (max). Tuning aid."""
 import sys; sys.path.insert(0, '.')
 import numpy as np, torch
 import paper_2405_20067_b200 as ndg
