@@ -52,8 +52,10 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     const int tid = threadIdx.x;
     const int64_t item = items[blockIdx.x];      // (tile << 32) | chunk, band order
     const int64_t t = item >> 32;
+    NDG_DCHECK(t >= 0 && t < T);
     const int64_t c = offsets[t] + (item & 0xffffffffLL) * kBwdChunk + tid;
     const bool active = c < offsets[t + 1];
+    NDG_DCHECK(tid > 0 || active);                 // every work item holds at least one candidate
 
     if (tid == 0) {
         mbar_init(&bar, 1);
@@ -70,6 +72,7 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
     int64_t e = 0;
     if (active) {
         e = idx[c];
+        NDG_DCHECK(e >= 0 && e < Gev);
         const float4* r4 = reinterpret_cast<const float4*>(rec + e * RS);
 #pragma unroll
         for (int v = 0; v < RS / 4; ++v) {

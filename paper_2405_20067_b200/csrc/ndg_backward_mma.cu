@@ -80,8 +80,10 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
     float* sM = reinterpret_cast<float*>(sQ + tile) + warp * 16 * 17;   // per-warp M^T scratch
     const int64_t item = items[blockIdx.x];   // (tile << 32) | chunk, band order (ndg_work_items)
     const int64_t t = item >> 32;
+    NDG_DCHECK(t >= 0 && t < T);
     const int64_t c0 = offsets[t] + (item & 0xffffffffLL) * kBwdChunk;
     const int64_t rem = offsets[t + 1] - c0;
+    NDG_DCHECK(rem > 0);
     const int n_here = rem < kBwdChunk ? (int)rem : kBwdChunk;
 
     const FxScales fx = fx_scales(bounds, (int64_t)T * tile);
@@ -115,6 +117,7 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
         for (int j = 0; j < kGpw; ++j) {
             live[j] = gb + j < n_here;
             e[j] = live[j] ? idx[c0 + gb + j] : 0;
+            NDG_DCHECK(e[j] >= 0 && e[j] < Gev);
             const float* r = rec_tc + e[j] * RT;
             auto at = [&](int i, int k) -> float {
                 return (live[j] && i < N && k < N) ? __ldg(r + ((k / 4) * N + i) * 4 + (k & 3)) : 0.f;

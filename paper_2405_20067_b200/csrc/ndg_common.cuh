@@ -147,6 +147,26 @@ struct DeviceOnce {
 };
 }  // namespace ndg
 
+// Bounds-checked build (make exp EXP="-DNDG_CHECKED" TAG=checked): device-side invariant checks on the
+// indices the kernels derive (candidate indices against Gev, CSR positions against the tile's range,
+// work items against the tile count, pre-filter cells and permutation slots); a failed check prints
+// the kernel, the condition and the block, and traps. Compiled out of the default build.
+#ifdef NDG_CHECKED
+#include <cstdio>
+#define NDG_DCHECK(cond)                                                                            \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("NDG_CHECKED %s:%d: %s failed (block %d, thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                              \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define NDG_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 // error string (per-thread) defined in ndg_prep.cu
 extern "C" void ndg_set_last_error(const char* msg);
 

@@ -220,6 +220,7 @@ __global__ void pf_scatter_kernel(int64_t Gev, int k, const double* __restrict__
         if (thr[e] < 0.0) continue;
         const int cell = cell_of(m_r[e], mn0, d0) * kNB + cell_of(m_r[Gev + e], mn1, d1);
         const int pos = start[cell] + atomicAdd(cursor + cell, 1);     // order inside a cell is irrelevant:
+        NDG_DCHECK(cell >= 0 && cell < kCells && pos >= start[cell] && pos < start[cell + 1]);
         perm[pos] = (int32_t)e;                                        // the mask is order-free
         for (int ri = 0; ri < k; ++ri) {
             ms[ri * Gev + pos] = m_r[ri * Gev + e];
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(256) pf_cull_kernel(int64_t T, int k, int64_t 
                 }
                 if (kept) {
                     const int e = perm[j];
+                    NDG_DCHECK(e >= 0 && e < Gev && j < start[kCells]);
                     atomicOr(mask + t * W + (e >> 5), 1u << (e & 31));
                     ++cnt;
                 }

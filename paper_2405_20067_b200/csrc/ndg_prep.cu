@@ -493,6 +493,7 @@ __global__ void __launch_bounds__(256) work_items_kernel(int64_t T, const int64_
             t = b0 + lo;
             c = cmin + (j - s_ex[lo]);
         }
+        NDG_DCHECK(t >= b0 && t < b1 && c >= 0 && c < chunk_off[t + 1] - chunk_off[t] && base + i < chunk_off[b1]);
         items[base + i] = (t << 32) | c;
     }
 }
@@ -631,8 +632,11 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(int64_t Gev, c
             const uint32_t wd = __shfl_sync(0xffffffffu, word, src);
             if (wd == 0u) continue;                               // warp-uniform
             const int64_t p = __shfl_sync(0xffffffffu, pos, src);
-            if ((wd >> lane) & 1u)
-                idx[p + __popc(wd & ((1u << lane) - 1u))] = (int32_t)((w0 + warp * 32 + src) * 32 + lane);
+            if ((wd >> lane) & 1u) {
+                const int64_t at = p + __popc(wd & ((1u << lane) - 1u));
+                NDG_DCHECK(at >= offsets[t] && at < offsets[t + 1] && (w0 + warp * 32 + src) * 32 + lane < Gev);
+                idx[at] = (int32_t)((w0 + warp * 32 + src) * 32 + lane);
+            }
         }
         __syncthreads();
         if (tid == 0) s_base += total;
