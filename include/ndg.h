@@ -270,6 +270,23 @@ int ndg_adam(int n, int64_t rows, float* params, const float* grad, float* m1, f
              int step, float lr_mean, float lr_chol, float lr_color, float lr_amp, float beta1, float beta2,
              float eps, void* stream);
 
+/*
+ * Device-side sample_batch: B fresh uniform queries in [0,1)^N sorted by the first
+ * dimension into contiguous tiles of `tile`, as the rows of the tiles t with t % world == rank (the
+ * rank's strided share of the global batch, in tile order). The sorted first coordinates are generated
+ * directly as uniform order statistics (normalised prefix sums of B + 1 exponentials, exact in 32.32
+ * fixed point, so non-decreasing by construction), the others iid; randomness is Philox4x32-10 keyed by
+ * (seed, draw), so a batch is a pure function of those two integers. B <= 2^24.
+ * workspace: ndg_sample_workspace(B) bytes of scratch.
+ */
+int64_t ndg_sample_workspace(int64_t B);
+int ndg_sample_batch(int n, int64_t B, int tile, int rank, int world, uint64_t seed, uint64_t draw, int64_t* workspace,
+                     float* queries, void* stream);
+
+/* shading_toy_target at queries[B][n] (4 <= n <= 10): params = freq[3] | phase[3];
+ * out[B][3] float32. */
+int ndg_shading_target(int n, int64_t B, const float* queries, const float* params, float* out, void* stream);
+
 /* FP32-pipe peak probe (roofline denominator for K5 / K7; not part of the reference interface):
  * `blocks` CTAs of 256 threads, each running 8 independent FFMA chains for 16 * iters steps. */
 int ndg_fp32_probe(float* out, int blocks, int iters, void* stream);

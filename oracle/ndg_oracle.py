@@ -770,3 +770,74 @@ def gbuffer_mixture(n: int, G: int, seed: int = 0, *, sigma0: float = 0.005, amp
 
 def synthetic_targets(B: int, seed: int = 3):
     return np.random.default_rng(seed).random((B, 3)).astype(np.float32)
+
+
+# ----------------------------------------------------------------------------------------------
+# device sampler and shading toy target; oracle copies of
+# csrc/ndg_sample.cu for the GPU parity tests (test infrastructure)
+# ----------------------------------------------------------------------------------------------
+_M0, _M1, _W0, _W1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57), 0x9E3779B9, 0xBB67AE85
+_U32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(c0, c1, c2, c3, k0, k1):
+    """Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11 -- the Random123 generator); vectorised over
+    counters. Pinned by the Random123 known-answer vectors in tests/test_oracle_kats.py."""
+    c = [np.asarray(x, np.uint64) & _U32 for x in (c0, c1, c2, c3)]
+    k0, k1 = int(k0) & 0xFFFFFFFF, int(k1) & 0xFFFFFFFF
+    for _ in range(10):
+        p0, p1 = _M0 * c[0], _M1 * c[2]
+        c = [(p1 >> np.uint64(32)) ^ c[1] ^ np.uint64(k0), p1 & _U32, (p0 >> np.uint64(32)) ^ c[3] ^ np.uint64(k1),
+             p0 & _U32]
+        k0, k1 = (k0 + _W0) & 0xFFFFFFFF, (k1 + _W1) & 0xFFFFFFFF
+    return [x.astype(np.uint32) for x in c]
+
+
+def _sample_key(seed: int, draw: int):
+    return seed & 0xFFFFFFFF, ((seed >> 32) ^ (draw >> 32)) & 0xFFFFFFFF
+
+
+def sample_spacings_fx(B: int, seed: int, draw: int) -> np.ndarray:
+    """The B + 1 exponential spacings E_i = -log(u_i) in 32.32 fixed point (int64), u_i a 53-bit
+    uniform in (0, 1] from Philox stream 0 at counter (i, 0, draw)."""
+    i = np.arange(B + 1, dtype=np.uint64)
+    k0, k1 = _sample_key(seed, draw)
+    r = philox4x32_10(i & _U32, i >> np.uint64(32), 0, draw & 0xFFFFFFFF, k0, k1)
+    u = ((r[0] >> 5).astype(np.float64) * 67108864.0 + (r[1] >> 6).astype(np.float64) + 1.0) / 9007199254740992.0
+    return np.rint(-np.log(u) * 4294967296.0).astype(np.int64)
+
+
+def sample_batch(n: int, B: int, tile: int, seed: int, draw: int, rank: int = 0, world: int = 1) -> np.ndarray:
+    """Oracle of ndg_sample_batch: the global batch sorted by dimension 0 (uniform order statistics
+    S_k / S_{B+1}, exact int64 prefix sums), other dimensions iid 24-bit uniforms from Philox streams
+    1, 3, 5, ... (four dimensions per call); returns the rows of the tiles t % world == rank."""
+    E = sample_spacings_fx(B, seed, draw)
+    S = np.cumsum(E)
+    x0 = np.minimum((S[:B].astype(np.float64) / float(S[B])).astype(np.float32), np.float32(0.99999994))
+    q = np.empty((B, n), np.float32)
+    q[:, 0] = x0
+    k = np.arange(B, dtype=np.uint64)
+    k0, k1 = _sample_key(seed, draw)
+    for d in range(1, n, 4):
+        r = philox4x32_10(k & _U32, k >> np.uint64(32), 1 + 2 * (d // 4), draw & 0xFFFFFFFF, k0, k1)
+        for j in range(4):
+            if d + j < n:
+                q[:, d + j] = (r[j] >> 8).astype(np.float32) * np.float32(1.0 / 16777216.0)
+    T = B // tile
+    return q.reshape(T, tile, n)[rank::world].reshape(-1, n)
+
+
+def shading_toy(q, freq, phase) -> np.ndarray:
+    """Oracle of ndg_shading_target / datasets.ShadingToyTarget in float64."""
+    q = np.asarray(q, np.float64)
+    n = q.shape[1]
+    pos = q[:, :3]
+    shade = 0.55 + 0.45 * np.prod(np.sin(2 * np.pi * np.asarray(freq) * pos + np.asarray(phase)), axis=1, keepdims=True)
+    alb = q[:, 6:9] if n >= 9 else np.full((q.shape[0], 3), 0.6)
+    rough = q[:, 9:10] if n >= 10 else np.full((q.shape[0], 1), 0.5)
+    v = np.concatenate([2.0 * q[:, 3:min(n, 6)] - 1.0, np.ones((q.shape[0], max(0, 6 - n)))], 1)
+    v = v / np.maximum(np.linalg.norm(v, axis=1, keepdims=True), 1e-6)
+    refl = np.stack([np.sin(2 * np.pi * pos[:, 0]), np.cos(2 * np.pi * pos[:, 1]), 0.5 + pos[:, 2]], 1)
+    refl = refl / np.linalg.norm(refl, axis=1, keepdims=True)
+    lobe = np.maximum((v * refl).sum(1, keepdims=True), 0.0) ** (2.0 + 40.0 * (1.0 - rough))
+    return alb * shade * 0.6 + 0.4 * lobe

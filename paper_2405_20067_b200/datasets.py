@@ -182,7 +182,9 @@ class ShadingToyTarget:
     """shading_toy_target: analytic shading-like function of
     position(3) | view direction(3) | albedo(3) | roughness(1) (first N of these roles, N in 4..10):
     a diffuse term smooth in position and modulated by albedo, plus a glossy cosine-power lobe around
-    a position-dependent reflection direction whose exponent falls to its minimum at roughness 1."""
+    a position-dependent reflection direction whose exponent falls to its minimum at roughness 1.
+    Evaluated by the `ndg_shading_target` kernel (csrc/ndg_sample.cu); the tests check it against the
+    oracle's float64 restatement."""
 
     def __init__(self, seed: int, n_dims: int):
         if not 4 <= n_dims <= 10:
@@ -191,48 +193,77 @@ class ShadingToyTarget:
         self.n_dims = n_dims
         self.freq = rng.uniform(1.0, 2.0, 3)
         self.phase = rng.uniform(0, 2 * np.pi, 3)
+        self._params = {}
 
     def __call__(self, q):
+        import ctypes
+
         import torch
-        n = self.n_dims
-        pos = q[:, :3]
-        f = torch.tensor(self.freq, device=q.device, dtype=q.dtype)
-        ph = torch.tensor(self.phase, device=q.device, dtype=q.dtype)
-        shade = 0.55 + 0.45 * torch.sin(2 * np.pi * f * pos + ph).prod(dim=1, keepdim=True)
-        alb = q[:, 6:9] if n >= 9 else torch.full((q.shape[0], 3), 0.6, device=q.device, dtype=q.dtype)
-        rough = q[:, 9:10] if n >= 10 else torch.full((q.shape[0], 1), 0.5, device=q.device, dtype=q.dtype)
-        if n >= 6:
-            v = 2.0 * q[:, 3:6] - 1.0
-        else:
-            v = torch.cat([2.0 * q[:, 3:n] - 1.0, torch.ones(q.shape[0], 6 - n, device=q.device, dtype=q.dtype)], 1)
-        v = v / v.norm(dim=1, keepdim=True).clamp_min(1e-6)
-        refl = torch.stack([torch.sin(2 * np.pi * pos[:, 0]), torch.cos(2 * np.pi * pos[:, 1]),
-                            0.5 + pos[:, 2]], 1)
-        refl = refl / refl.norm(dim=1, keepdim=True)
-        expo = 2.0 + 40.0 * (1.0 - rough)
-        lobe = (v * refl).sum(1, keepdim=True).clamp_min(0.0) ** expo
-        return (alb * shade * 0.6 + 0.4 * lobe).to(torch.float32)
+
+        from . import kernels as K
+        q = q.contiguous().float()
+        p = self._params.get(q.device)
+        if p is None:
+            p = torch.tensor(np.concatenate([self.freq, self.phase]), dtype=torch.float32, device=q.device)
+            self._params[q.device] = p
+        out = torch.empty(q.shape[0], 3, dtype=torch.float32, device=q.device)
+        K.call("ndg_shading_target", self.n_dims, int(q.shape[0]), ctypes.c_void_p(q.data_ptr()),
+               ctypes.c_void_p(p.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+               ctypes.c_void_p(torch.cuda.current_stream(q.device).cuda_stream))
+        return out
 
 
-def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, generator, device, rank: int = 0,
+class QuerySampler:
+    """The stream of training batches: a counter-based generator (Philox4x32-10 keyed by seed, one draw
+    index per batch) on the device, so its whole state is (seed, draw) -- checkpointed as two integers --
+    and every rank of a data-parallel fit draws the same global batch."""
+
+    def __init__(self, seed: int, draw: int = 0):
+        self.seed, self.draw = int(seed) & ((1 << 64) - 1), int(draw)
+        self._ws = None
+
+    def state(self) -> dict:
+        return dict(seed=self.seed, draw=self.draw)
+
+    def set_state(self, st: dict):
+        self.seed, self.draw = int(st["seed"]), int(st["draw"])
+
+    def queries(self, n_dims: int, batch_size: int, tile_size: int, device, rank: int = 0, world: int = 1):
+        """The next global batch, this rank's strided tiles of it."""
+        import ctypes
+
+        import torch
+
+        from . import kernels as K
+        T = batch_size // tile_size
+        mine = len(range(rank, T, world))
+        q = torch.empty(mine * tile_size, n_dims, dtype=torch.float32, device=device)
+        nb = int(K.load().ndg_sample_workspace(batch_size))
+        if self._ws is None or self._ws.numel() * 8 < nb or self._ws.device != q.device:
+            self._ws = torch.empty((nb + 7) // 8, dtype=torch.int64, device=device)
+        K.call("ndg_sample_batch", n_dims, batch_size, tile_size, rank, world, ctypes.c_uint64(self.seed),
+               ctypes.c_uint64(self.draw), ctypes.c_void_p(self._ws.data_ptr()), ctypes.c_void_p(q.data_ptr()),
+               ctypes.c_void_p(torch.cuda.current_stream(q.device).cuda_stream))
+        self.draw += 1
+        return q
+
+
+def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, sampler, device, rank: int = 0,
                  world: int = 1):
-    """SPEC.md:440-448 on the device: fresh uniform queries, stable-sorted by the first (position)
-    dimension into contiguous tiles, exact targets. batch_size must be a multiple of tile_size.
+    """SPEC.md:440-448 on the device: fresh uniform queries, sorted by the first (position) dimension
+    into contiguous tiles, exact targets. batch_size must be a multiple of tile_size. `sampler` is a
+    QuerySampler (or an int seed for a one-off batch); the sort is generated, not performed
+    (csrc/ndg_sample.cu: the sorted first coordinates are uniform order statistics).
 
-    Data-parallel (world > 1): every rank draws the same GLOBAL batch from identically seeded
-    generators and keeps its strided tiles (global tile i -> rank i mod world, parallel.shard_tiles),
-    evaluating the target only there -- so the union over ranks is exactly the 1-GPU batch and the
-    summed gradients equal the 1-GPU step's."""
-    import torch
+    Data-parallel (world > 1): every rank draws the same GLOBAL batch and keeps its strided tiles (global
+    tile i -> rank i mod world, parallel.shard_tiles), evaluating the target only there -- so the union
+    over ranks is exactly the 1-GPU batch and the summed gradients equal the 1-GPU step's."""
     if batch_size % tile_size:
         raise ValueError("batch_size must be a multiple of tile_size (SPEC.md:441)")
-    q = torch.rand(batch_size, n_dims, generator=generator, device=device)
-    order = torch.sort(q[:, 0], stable=True).indices
-    q = q[order]
-    if world > 1:
-        T = batch_size // tile_size
-        if T < world:
-            raise ValueError(f"{T} tiles cannot give each of {world} ranks one (batch_size / tile_size >= world)")
-        q = q.view(T, tile_size, n_dims)[rank::world].reshape(-1, n_dims)
-    q = q.contiguous()
+    T = batch_size // tile_size
+    if world > 1 and T < world:
+        raise ValueError(f"{T} tiles cannot give each of {world} ranks one (batch_size / tile_size >= world)")
+    if not isinstance(sampler, QuerySampler):
+        sampler = QuerySampler(int(sampler))
+    q = sampler.queries(n_dims, batch_size, tile_size, device, rank, world)
     return q, target(q).contiguous()

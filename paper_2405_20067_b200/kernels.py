@@ -57,6 +57,9 @@ SIGNATURES = {
     "ndg_adam": [_I, _L, _P, _P, _P, _P, _P, _I, _F, _F, _F, _F, _F, _F, _F, _P],
     "ndg_tc_records": [_I, _L, _P, _P, _P, _P, _P, _P, _P],
     "ndg_forward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _F, _L, _P, _P, _P, _P],
+    "ndg_sample_workspace": [_L],
+    "ndg_sample_batch": [_I, _L, _I, _I, _I, C.c_uint64, C.c_uint64, _P, _P, _P],
+    "ndg_shading_target": [_I, _L, _P, _P, _P, _P],
     "ndg_fp32_probe": [_P, _I, _I, _P],
     "ndg_fp32_probe_flops": [_I, _I],
     "ndg_tf32_probe": [_P, _I, _I, _P],
@@ -90,7 +93,8 @@ def load():
         fn.argtypes = argtypes
         fn.restype = {"ndg_last_error": C.c_char_p, "ndg_fp32_probe_flops": C.c_double,
                       "ndg_tf32_probe_flops": C.c_double, "ndg_hmma_probe_flops": C.c_double,
-                      "ndg_cull_prefilter_workspace": C.c_int64}.get(name, C.c_int)
+                      "ndg_cull_prefilter_workspace": C.c_int64,
+                      "ndg_sample_workspace": C.c_int64}.get(name, C.c_int)
     _lib = lib
     return lib
 
@@ -102,11 +106,11 @@ class NdgLaunchError(RuntimeError):
 # entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
 LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_cull_prefilter", "ndg_scan_counts",
              "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_loss_rel_l2", "ndg_backward", "ndg_backward_mma",
-             "ndg_work_items", "ndg_bwd_bounds", "ndg_acc_dequant", "ndg_active_mask", "ndg_centre_records", "ndg_loss_f64", "ndg_backward_f64", "ndg_fd_f64", "ndg_nonfinite_query", "ndg_epilogue", "ndg_adam",
+             "ndg_work_items", "ndg_bwd_bounds", "ndg_acc_dequant", "ndg_active_mask", "ndg_centre_records", "ndg_loss_f64", "ndg_backward_f64", "ndg_fd_f64", "ndg_nonfinite_query", "ndg_sample_batch", "ndg_shading_target", "ndg_epilogue", "ndg_adam",
              "ndg_fp32_probe", "ndg_tf32_probe", "ndg_hmma_probe"}
 # entry points that enqueue several kernels: ndg_cull_prefilter = init, stats, hist, plan, scatter, zero,
 # pre-filtered cull and the dense cull (the plan makes one of the two paths exit at once)
-MULTI_LAUNCH = {"ndg_cull_prefilter": 8}
+MULTI_LAUNCH = {"ndg_cull_prefilter": 8, "ndg_sample_batch": 3}
 launch_count = 0
 
 

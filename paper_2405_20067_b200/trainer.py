@@ -122,17 +122,18 @@ class Trainer:
                  allreduce=None, rank: int = 0, world: int = 1):
         self.cfg, self.target, self.n = cfg, target, n_dims
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        # the sampling generator is seeded identically on every rank: each draws the same global batch
-        # and keeps its own tiles (datasets.sample_batch), so the ranks' tiles partition the 1-GPU batch
-        self.gen = torch.Generator(device=self.device)
-        self.gen.manual_seed(cfg.seed * 1000003)
+        # the batch stream (counter-based, device-side) is seeded identically on every rank: each draws
+        # the same global batch and keeps its own tiles (datasets.sample_batch), so the ranks' tiles
+        # partition the 1-GPU batch
+        self.sampler = D.QuerySampler(cfg.seed * 1000003 + 1)
         self.rng = np.random.default_rng(cfg.seed)
         self.allreduce, self.rank, self.world = allreduce, rank, world
         if mixture is None:
-            q0, _ = D.sample_batch(target, n_dims, max(cfg.tile_size, cfg.n_components), 1, self._init_gen(),
-                                   self.device)
-            mixture = initial_mixture(cfg, n_dims, q0[torch.randperm(q0.shape[0], generator=self._init_gen(),
-                                                                     device=self.device)], self.device)
+            # initial means from data points: a one-off draw, identical on every rank; the
+            # first coordinate of a sorted draw is ordered, so pick the points by a seeded permutation
+            q0 = D.QuerySampler(cfg.seed).queries(n_dims, max(cfg.tile_size, cfg.n_components), 1, self.device)
+            perm = np.random.default_rng(cfg.seed).permutation(q0.shape[0])
+            mixture = initial_mixture(cfg, n_dims, q0[torch.from_numpy(perm).to(self.device)], self.device)
         self.mix = mixture
         self.ids = torch.arange(self.mix.G, dtype=torch.int64, device=self.device)
         self.next_id = self.mix.G
@@ -146,16 +147,11 @@ class Trainer:
         self.phase_stats = None       # [Gev, 3] float64 on the device: the phase's density statistics
         self.last_good = self.mix.clone()
 
-    def _init_gen(self):
-        g = torch.Generator(device=self.device)
-        g.manual_seed(self.cfg.seed)           # identical initial mixture on every rank
-        return g
-
     # -- one iteration -----------------------------------------------------------------------
     def iteration(self) -> MetricsRow:
         cfg = self.cfg
         t0 = time.perf_counter()
-        q, tg = D.sample_batch(self.target, self.n, cfg.batch_size, cfg.tile_size, self.gen, self.device,
+        q, tg = D.sample_batch(self.target, self.n, cfg.batch_size, cfg.tile_size, self.sampler, self.device,
                                self.rank, self.world)
         res = self.hp.fwd_bwd(self.mix, q, tg, cull=cfg.cull, n_total=cfg.batch_size, allreduce=self.allreduce)
         self.last_allreduce_bytes = res.grads.reduced().numel() * 4 if self.allreduce is not None else 0
@@ -180,14 +176,13 @@ class Trainer:
 
     # -- resume state (resume is bit-identical) ----------------------------
     def rng_state(self) -> dict:
-        """Everything random that the future of the fit depends on: the torch sampling generator
+        """Everything random that the future of the fit depends on: the batch stream's (seed, draw)
         (identical on every rank) and the full numpy PCG64 state of the spawn RNG."""
-        return dict(seed=self.cfg.seed, torch=[int(b) for b in self.gen.get_state().tolist()],
-                    numpy=self.rng.bit_generator.state)
+        return dict(seed=self.cfg.seed, sampler=self.sampler.state(), numpy=self.rng.bit_generator.state)
 
     def set_rng_state(self, st: dict):
-        if "torch" in st:
-            self.gen.set_state(torch.tensor(st["torch"], dtype=torch.uint8))
+        if isinstance(st.get("sampler"), dict):
+            self.sampler.set_state(st["sampler"])
         if isinstance(st.get("numpy"), dict):
             self.rng.bit_generator.state = st["numpy"]
 
@@ -371,9 +366,7 @@ def train(cfg: TrainConfig, target, n_dims: int, *, mixture: Mixture | None = No
 
 def held_out_rel_l2(mix: Mixture, target, n_dims: int, n: int = 1 << 14, seed: int = 12345, tile_size: int = 256):
     """Relative L2 of the mixture against the target on fresh held-out queries."""
-    g = torch.Generator(device=mix.device)
-    g.manual_seed(seed)
-    q, tg = D.sample_batch(target, n_dims, n, tile_size, g, mix.device)
+    q, tg = D.sample_batch(target, n_dims, n, tile_size, D.QuerySampler(seed), mix.device)
     hp = HotPath(n_dims, tile_size=tile_size, device=mix.device)
     pred = hp.evaluate(mix, q, cull=True)
     return float(torch.linalg.norm(pred - tg) / torch.linalg.norm(tg))

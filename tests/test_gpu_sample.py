@@ -1,0 +1,71 @@
+"""The device-side batch sampler and shading-toy target (csrc/ndg_sample.cu) against
+the oracle: the Philox streams bit-exact, the order-statistics first coordinate within one float32 ulp
+(the kernel's float64 log may differ from NumPy's in the last place), rank slices, determinism and the
+shading function within float32 tolerance."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ndg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _D():
+    from paper_2405_20067_b200 import datasets as D
+    return D
+
+
+@pytest.mark.parametrize("n,B,tile,seed,draw", [(4, 4096, 256, 1, 0), (10, 1 << 16, 256, 7, 3),
+                                                (16, 3 * 1000, 250, 2 ** 40 + 5, 2 ** 33 + 1),
+                                                (6, 256 * 4103, 256, 123, 9)])
+def test_sampler_matches_oracle(cuda, n, B, tile, seed, draw):
+    """B = 256 * 4103 > 2^20 spans more than one pass of the block-sum scan; the 64-bit seed / draw case
+    exercises the key's high words."""
+    D = _D()
+    q = D.QuerySampler(seed, draw).queries(n, B, tile, "cuda").cpu().numpy()
+    ref = O.sample_batch(n, B, tile, seed, draw)
+    assert q.shape == ref.shape
+    assert np.array_equal(q[:, 1:], ref[:, 1:])                               # integer streams: exact
+    ulp = np.spacing(np.maximum(np.abs(ref[:, 0]), np.float32(1e-30)))
+    assert np.all(np.abs(q[:, 0] - ref[:, 0]) <= ulp)
+    assert np.all(np.diff(q[:, 0]) >= 0) and q.min() >= 0 and q.max() < 1    # sorted tiles in [0, 1)
+
+
+def test_sampler_rank_slices_and_determinism(cuda):
+    D = _D()
+    B, tile, n = 1 << 14, 256, 8
+    full = D.QuerySampler(5, 2).queries(n, B, tile, "cuda")
+    again = D.QuerySampler(5, 2).queries(n, B, tile, "cuda")
+    assert torch.equal(full, again)
+    T = B // tile
+    for world in (2, 3, 8):
+        for r in range(world):
+            part = D.QuerySampler(5, 2).queries(n, B, tile, "cuda", r, world)
+            assert torch.equal(part, full.view(T, tile, n)[r::world].reshape(-1, n))
+    s = D.QuerySampler(5)
+    a, b = s.queries(n, B, tile, "cuda"), s.queries(n, B, tile, "cuda")
+    assert s.state() == {"seed": 5, "draw": 2} and not torch.equal(a, b)
+    assert torch.equal(b, D.QuerySampler(5, 1).queries(n, B, tile, "cuda"))
+
+
+def test_sample_batch_targets_and_errors(cuda):
+    D = _D()
+    tgt = D.ShadingToyTarget(0, 6)
+    q, t = D.sample_batch(tgt, 6, 2048, 256, D.QuerySampler(4), "cuda", rank=1, world=2)
+    assert q.shape == (1024, 6) and t.shape == (1024, 3)
+    with pytest.raises(ValueError):
+        D.sample_batch(tgt, 6, 2000, 256, 4, "cuda")
+    with pytest.raises(ValueError):
+        D.sample_batch(tgt, 6, 512, 256, 4, "cuda", rank=0, world=4)
+
+
+@pytest.mark.parametrize("n", [4, 5, 6, 8, 9, 10])
+def test_shading_target_matches_oracle(cuda, n):
+    D = _D()
+    tgt = D.ShadingToyTarget(3, n)
+    q = D.QuerySampler(8).queries(n, 1 << 15, 256, "cuda")
+    got = tgt(q).cpu().numpy()
+    ref = O.shading_toy(q.cpu().numpy(), tgt.freq, tgt.phase)
+    assert got.shape == (1 << 15, 3) and got.dtype == np.float32
+    assert np.max(np.abs(got - ref)) < 2e-5, np.max(np.abs(got - ref))

@@ -31,8 +31,7 @@ def test_recovery_and_refinement(cuda):
     cfg = T.TrainConfig(iterations=3000, phase_length=300, n_components=32, batch_size=4096, seed=1)
     tr = T.Trainer(cfg, tgt, 6)
     e0 = T.held_out_rel_l2(tr.mix, tgt, 6)
-    g = torch.Generator(device="cuda")
-    g.manual_seed(99)
+    g = D.QuerySampler(99)
     vq, vt = D.sample_batch(tgt, 6, 4096, 256, g, "cuda")
     events, spikes = [], []
     for it in range(cfg.iterations):
@@ -61,8 +60,7 @@ def test_materialize_event_preserves_output(cuda):
     ch[5, R - 1] = float(np.log(0.05))                                  # activated amp 0.05 >= t = 0.01
     ch[5, :4] = torch.tensor([0.05, -0.02, 0.03, 0.01])
     tr.mix.child = ch
-    g = torch.Generator(device="cuda")
-    g.manual_seed(3)
+    g = D.QuerySampler(3)
     q, _ = D.sample_batch(tgt, 4, 4096, 256, g, "cuda")
     before = tr.hp.evaluate(tr.mix, q, cull=False)
     ev = tr.materialize_step()
@@ -82,8 +80,7 @@ def test_no_spike_shading_toy(cuda):
     tgt = D.ShadingToyTarget(0, 10)
     cfg = T.TrainConfig(iterations=1500, phase_length=300, n_components=1024, batch_size=16384, seed=2)
     tr = T.Trainer(cfg, tgt, 10)
-    g = torch.Generator(device="cuda")
-    g.manual_seed(7)
+    g = D.QuerySampler(7)
     vq, vt = D.sample_batch(tgt, 10, 16384, 256, g, "cuda")
     spikes = []
     for it in range(cfg.iterations):
@@ -104,9 +101,7 @@ def test_gmm_target_any_batch_and_component_count(cuda):
     unpadded evaluation of the same queries."""
     D, T = _T()
     tgt = D.GmmOracleTarget(0, 4, 6)
-    g = torch.Generator(device="cuda")
-    g.manual_seed(1)
-    q = torch.rand(300, 4, generator=g, device="cuda")
+    q = torch.rand(300, 4, generator=torch.Generator(device="cuda").manual_seed(1), device="cuda")
     p300 = tgt(q)
     p512 = tgt(torch.cat([q, q[:212]]))
     assert p300.shape == (300, 3) and torch.equal(p300, p512[:300])
@@ -172,8 +167,7 @@ def test_frozen_rows_are_compacted_and_checkpointed_in_place(cuda, tmp_path):
     fl = fm.flags.cpu().numpy()
     assert all(fl[i] & FLAG_FROZEN for i in (3, 10, 20))
     assert fm.G == full.mix.G + full.archive["ids"].numel()
-    g = torch.Generator(device="cuda")
-    g.manual_seed(2)
+    g = D.QuerySampler(2)
     q, _ = D.sample_batch(tgt, 4, 2048, 256, g, "cuda")
     a = full.hp.evaluate(full.mix, q, cull=False)
     b = full.hp.evaluate(fm, q, cull=False)

@@ -340,3 +340,36 @@ def test_adam_kats():
     for s in range(1, 501):
         x, m1, m2 = O.adam_step(x, 2 * (x - 1.0), m1, m2, s, 1e-2)
     assert abs(x[0] - 1.0) < 0.05
+
+
+@pytest.mark.parametrize("ctr,key,want", [
+    ((0, 0, 0, 0), (0, 0), "6627e8d5 e169c58d bc57ac4c 9b00dbd8"),
+    ((0xFFFFFFFF,) * 4, (0xFFFFFFFF, 0xFFFFFFFF), "408f276d 41c83b0e a20bc7c6 6d5451fd"),
+    ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+     "d16cfe09 94fdcceb 5001e420 24126ea1"),
+])
+def test_philox_random123_kats(ctr, key, want):
+    """The sampler's Philox4x32-10 against the published Random123 known-answer vectors
+    (kat_vectors: philox4x32 10 ...), which pins the oracle the GPU sampler is checked against."""
+    r = O.philox4x32_10(*[[c] for c in ctr], *key)
+    assert " ".join(f"{int(x[0]):08x}" for x in r) == want
+
+
+def test_sampler_oracle_distribution():
+    """sample_batch's order-statistics construction: dimension 0 is non-decreasing and, as a set,
+    uniform on [0, 1) (Kolmogorov-Smirnov); the other dimensions are iid uniform; rank slices
+    partition the global batch."""
+    B, n = 1 << 15, 7
+    q = O.sample_batch(n, B, 256, seed=11, draw=5)
+    assert np.all(np.diff(q[:, 0]) >= 0) and q.min() >= 0 and q.max() < 1
+    grid = (np.arange(B) + 0.5) / B
+    for d in range(n):
+        ks = np.max(np.abs(np.sort(q[:, d]) - grid))
+        assert ks < 1.63 / math.sqrt(B), (d, ks)                    # 1% KS critical value
+    parts = [O.sample_batch(n, B, 256, 11, 5, r, 3) for r in range(3)]
+    T = B // 256
+    back = np.empty_like(q).reshape(T, 256, n)
+    for r in range(3):
+        back[r::3] = parts[r].reshape(-1, 256, n)
+    assert np.array_equal(back.reshape(B, n), q)
+    assert not np.array_equal(O.sample_batch(n, 4096, 256, 11, 6), O.sample_batch(n, 4096, 256, 11, 5))

@@ -27,9 +27,7 @@ dev = torch.device("cuda", 0)
 
 
 def held_out(mix, target, n, count=1 << 14):
-    g = torch.Generator(device=dev)
-    g.manual_seed(12345)
-    q, tg = D.sample_batch(target, n, count, 256, g, dev)
+    q, tg = D.sample_batch(target, n, count, 256, D.QuerySampler(12345), dev)
     pred = HotPath(n, device=dev).evaluate(mix, q, cull=True)
     rel = float(torch.linalg.norm(pred - tg) / torch.linalg.norm(tg))
     mse = float(torch.mean((pred - tg) ** 2))
