@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--tile", type=int, default=256)
     ap.add_argument("--k", type=int, default=16)
     ap.add_argument("--children", action="store_true", help="every component carries a live child (Gev = 2G)")
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="replay the step as one CUDA graph (auto: when the worst-case candidate list is <= 2^24)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the regime-C secondary measurement")
@@ -314,10 +316,23 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
     n_total = a.batch * world
     allreduce = P.make_allreduce() if world > 1 else None
     it = [0]
+    # small, launch-bound steps (worst-case candidate list <= 2^24 entries, e.g. cfg1) replay one CUDA
+    # graph of K1..K8 (engine.GraphedStep); qd / td are then its input buffers
+    gs = None
+    if a.graph == "on" or (a.graph == "auto" and ndg.GraphedStep.eligible(hp, mix, qd.shape[0])):
+        hp.enable_kernel_timing(True)                   # capture the K4 / K5 / K7 event pairs too
+        gs = ndg.GraphedStep(hp, mix, qd, td, n_total=n_total, grads=grads)
+        hp.enable_kernel_timing(False)
 
     def step(queries, targets):
         it[0] += 1
-        res = hp.fwd_bwd(mix, queries, targets, n_total=n_total, grads=grads, allreduce=allreduce)
+        if gs is not None:
+            if queries is not qd:
+                qd.copy_(queries, non_blocking=True)
+                td.copy_(targets, non_blocking=True)
+            res = gs(allreduce=allreduce)
+        else:
+            res = hp.fwd_bwd(mix, queries, targets, n_total=n_total, grads=grads, allreduce=allreduce)
         ndg.adam_step(mix, grads, state, step=it[0])
         return res
 
@@ -350,7 +365,7 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
         clocks.end()
     if world > 1:
         dist.barrier()
-    launches = K.launch_count - launches0
+    launches = K.launch_count - launches0 + (gs.launches * steps if gs is not None else 0)
     clk = clocks.stop() if clocks else None
     fwd_ms = statistics.mean(hp.kernel_ms("forward"))
     bwd_ms = statistics.mean(hp.kernel_ms("backward"))
@@ -367,7 +382,7 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
                cull_ms=cull_ms, prefilter_ran=bool(plan and plan[1]),
                allreduce_bytes=int(grads.reduced().numel()) * 4,
                launches=launches, clocks=clk, loss=res.loss, sigma0=s0, fwd_impl=hp.last_forward_impl,
-               bwd_impl=hp.last_backward_impl)
+               bwd_impl=hp.last_backward_impl, graph=gs is not None and not gs.stale)
 
     # K4 alone, dense pass vs bucket pre-filter (same tile and projected bounds; identical masks)
     recs = hp.activate(mix)
@@ -391,9 +406,14 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             flush.zero_()
             e0.record()
-            qd2 = qh.to(dev, non_blocking=True)
-            td2 = th.to(dev, non_blocking=True)
-            res = step(qd2, td2)                       # fwd_bwd reads the loss back to the host
+            if gs is not None:                         # H2D straight into the graph's input buffers
+                qd.copy_(qh, non_blocking=True)
+                td.copy_(th, non_blocking=True)
+                res = step(qd, td)
+            else:
+                qd2 = qh.to(dev, non_blocking=True)
+                td2 = th.to(dev, non_blocking=True)
+                res = step(qd2, td2)                   # fwd_bwd reads the loss back to the host
             e1.record()
             e1.synchronize()
             if i >= warmup:
@@ -490,6 +510,40 @@ def our_arm(a, rank, world):
     except (OSError, ValueError):
         pass
     step_tflops = pairs * ndg.kept_pairs_flops(n) / (main["ms_per_step"] * 1e-3) / 1e12
+    if dom == "forward" and main["fwd_impl"] == "tc":
+        f = kern["forward"]
+        roof = dict(bound="tensor", kernel=dom, achieved=f["tensor_tflops_algorithmic"], peak=tpeak, unit="TFLOP/s",
+                    frac=f["frac_of_measured_tf32_algorithmic"], traffic=traffic,
+                    peak_source="measured tcgen05 kind::tf32 probe on this GPU",
+                    bound_note="the dominant kernel is the tcgen05 K5: achieved counts the algorithmic z-GEMM "
+                               "(2(N+1)N flops per pair) once; 3xTF32 issues it three times (kernels.forward)",
+                    flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n)),
+                    step_fp32_equivalent_tflops=step_tflops)
+    else:
+        roof = (dict(bound="tensor", kernel=dom, achieved=kern[dom]["tensor_tflops"],
+             peak=kern[dom]["tensor_peak_measured"], unit="TFLOP/s",
+             frac=kern[dom]["frac_of_measured_hmma"], traffic=traffic,
+             peak_source="measured mma.sync m16n8k8 tf32 probe (ndg_hmma_probe) on this GPU: the legacy "
+                         "warp-level tensor path this kernel issues, not the tcgen05 peak",
+             bound_note="the dominant kernel is the warp-MMA K7 (N >= 15): achieved counts its padded "
+                        "3xTF32 MMA flops (2176 per pair); its FP32-equivalent rate is in kernels.backward",
+             flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n),
+                                 backward_tensor=kern[dom]["tensor_flops_per_pair"]),
+             step_fp32_equivalent_tflops=step_tflops)
+        if dom == "backward" and main["bwd_impl"] == "mma" else
+        dict(bound="fp32", kernel=dom, achieved=kern[dom]["tflops"], peak=peak, unit="TFLOP/s",
+            frac=kern[dom]["tflops"] / peak, traffic=traffic,
+            peak_source="measured FFMA probe (ndg_fp32_probe) on this GPU; MEASURED_PEAKS.json has no "
+                        "FP32 entry",
+            bound_note="the dominant kernel (K7 backward) runs on the FP32 SIMT pipe: its DRAM traffic "
+                       "(`traffic`, ncu, ~2x its algorithmic bytes) is <1% of the HBM roof and it issues "
+                       "no tensor-core work, so neither 'hbm' nor 'tensor' applies; the K5 forward's "
+                       "tensor roofline is in kernels.forward",
+            peak_nominal=NOMINAL_FP32_TFLOPS, frac_of_nominal=kern[dom]["tflops"] / NOMINAL_FP32_TFLOPS,
+            flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n)),
+            step_fp32_equivalent_tflops=step_tflops,
+            step_note="the step's rate counts K5's tensor-core z-GEMM as FP32-equivalent flops; the "
+                      "roofline figure of the step is `frac` (its dominant kernel, K7)"))
     line = dict(
         metric=METRIC, value=main["value"], unit="queries/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
         ms_per_step=main["ms_per_step"], higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f32",
@@ -499,34 +553,14 @@ def our_arm(a, rank, world):
                     global_batch=a.batch * world, tile=a.tile, k=a.k, multiplier=3.0, regime=a.regime,
                     kept_fraction=main["kept"], pairs_per_step=pairs, sigma0=main["sigma0"],
                     allreduce_payload_bytes_per_step=main["allreduce_bytes"],
+                    step_launch=("one CUDA-graph replay of K1..K8 per step (engine.GraphedStep; worst-case-sized "
+                                 "candidate list, no mid-step read-back) + K9 Adam" if main["graph"] else
+                                 "eager: one C-ABI launch per stage, one mid-step read-back sizing the candidate list"),
                     l2="flushed before every timed step (256 MiB write, outside the timed interval)",
                     parallelism=f"dp{world} (one global batch of {a.batch * world} queries, strided tiles per "
                                 f"rank, mixture replicated, 1 {(dist.get_backend() if dist else 'nccl').upper()} "
                                 f"allreduce/step of the flat gradient buffer)"),
-        roofline=(dict(bound="tensor", kernel=dom, achieved=kern[dom]["tensor_tflops"],
-                       peak=kern[dom]["tensor_peak_measured"], unit="TFLOP/s",
-                       frac=kern[dom]["frac_of_measured_hmma"], traffic=traffic,
-                       peak_source="measured mma.sync m16n8k8 tf32 probe (ndg_hmma_probe) on this GPU: the legacy "
-                                   "warp-level tensor path this kernel issues, not the tcgen05 peak",
-                       bound_note="the dominant kernel is the warp-MMA K7 (N >= 15): achieved counts its padded "
-                                  "3xTF32 MMA flops (2176 per pair); its FP32-equivalent rate is in kernels.backward",
-                       flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n),
-                                           backward_tensor=kern[dom]["tensor_flops_per_pair"]),
-                       step_fp32_equivalent_tflops=step_tflops)
-                  if dom == "backward" and main["bwd_impl"] == "mma" else
-                  dict(bound="fp32", kernel=dom, achieved=kern[dom]["tflops"], peak=peak, unit="TFLOP/s",
-                      frac=kern[dom]["tflops"] / peak, traffic=traffic,
-                      peak_source="measured FFMA probe (ndg_fp32_probe) on this GPU; MEASURED_PEAKS.json has no "
-                                  "FP32 entry",
-                      bound_note="the dominant kernel (K7 backward) runs on the FP32 SIMT pipe: its DRAM traffic "
-                                 "(`traffic`, ncu, ~2x its algorithmic bytes) is <1% of the HBM roof and it issues "
-                                 "no tensor-core work, so neither 'hbm' nor 'tensor' applies; the K5 forward's "
-                                 "tensor roofline is in kernels.forward",
-                      peak_nominal=NOMINAL_FP32_TFLOPS, frac_of_nominal=kern[dom]["tflops"] / NOMINAL_FP32_TFLOPS,
-                      flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n)),
-                      step_fp32_equivalent_tflops=step_tflops,
-                      step_note="the step's rate counts K5's tensor-core z-GEMM as FP32-equivalent flops; the "
-                                "roofline figure of the step is `frac` (its dominant kernel, K7)")),
+        roofline=roof,
         kernels=dict(kern, cull=kern_cull), gpu_launches=main["launches"], clocks=main["clocks"], loss=main["loss"],
     )
     if "e2e" in main:

@@ -177,7 +177,8 @@ int ndg_bwd_bounds(int n, int64_t B, const float* qrec, int64_t Gev, const float
  * statistics S, t, gA and the density-control statistics, then adds them to accum[2][Gev][A] (int64
  * fixed point: hi words then lo words, zeroed by the caller) with scales derived from `bounds`. The
  * sums are exact integers, so the result is independent of the order work items run in (SPEC.md:294,
- * bit-reproducible training :380, :581). `items` from ndg_work_items.
+ * bit-reproducible training :380, :581). `items` from ndg_work_items; n_chunks may exceed the real
+ * count (a worst-case-sized list for CUDA-graph replay) when the extra slots hold -1, which exit.
  */
 int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec, int centred, const int64_t* offsets,
                  const int32_t* idx, const int64_t* items, int64_t n_chunks, int64_t Gev, const uint32_t* bounds,

@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
 
     const int tid = threadIdx.x;
     const int64_t item = items[blockIdx.x];      // (tile << 32) | chunk, band order
+    if (item < 0) return;                        // unused slot of a worst-case-sized list (graph replay)
     const int64_t t = item >> 32;
     NDG_DCHECK(t >= 0 && t < T);
     const int64_t c = offsets[t] + (item & 0xffffffffLL) * kBwdChunk + tid;

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
     const int gid = lane >> 2, tig = lane & 3, odd = gid & 1;
     float* sM = reinterpret_cast<float*>(sQ + tile) + warp * 16 * 17;   // per-warp M^T scratch
     const int64_t item = items[blockIdx.x];   // (tile << 32) | chunk, band order (ndg_work_items)
+    if (item < 0) return;                        // unused slot of a worst-case-sized list (graph replay)
     const int64_t t = item >> 32;
     NDG_DCHECK(t >= 0 && t < T);
     const int64_t c0 = offsets[t] + (item & 0xffffffffLL) * kBwdChunk;

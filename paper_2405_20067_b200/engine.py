@@ -263,6 +263,9 @@ class HotPath:
         self.last_forward_impl = self.last_backward_impl = None   # what the last step ran
         self.last_centred = False
         self.events = None   # when a dict: {"forward": [(start, end), ...], "backward": [...]} CUDA events
+        # GraphedStep capture: the conditioning read-back is replaced by the captured value and the
+        # candidate list / K7 work items are sized for the worst case, so no stage reads back mid-step
+        self._static = None
 
     def enable_kernel_timing(self, on: bool = True):
         """Record CUDA events on the launching stream around the K5 and K7 launches."""
@@ -271,7 +274,8 @@ class HotPath:
     def _ev(self, name, when):
         if self.events is None:
             return
-        e = torch.cuda.Event(enable_timing=True)
+        # under graph capture: event record nodes, re-recorded by every replay (GraphedStep reads them)
+        e = torch.cuda.Event(enable_timing=True, external=self._static is not None)
         e.record()
         if when == 0:
             self.events[name].append([e, None])
@@ -281,7 +285,7 @@ class HotPath:
     def kernel_ms(self, name):
         """Per-launch durations (ms) of the recorded launches of K5 ("forward"), K7 ("backward") and the
         K4a / K4p cull mask ("cull")."""
-        return [a.elapsed_time(b) for a, b in self.events[name]]
+        return [x[0] if len(x) == 1 else x[0].elapsed_time(x[1]) for x in self.events[name]]
 
     # -- K1 --------------------------------------------------------------------------------
     def activate(self, mix: Mixture) -> EvalRecords:
@@ -301,6 +305,8 @@ class HotPath:
         cond = torch.zeros(3, dtype=torch.float64, device=dev)
         K.call("ndg_tc_records", n, Gev, _p(mean64), _p(chol64), _p(eflags), _p(rec), _p(rec_tc), _p(cond), _stream())
         recs = EvalRecords(Gev, rec, mean64, chol64, eflags, rec_tc, cond)
+        if self._static is not None:
+            recs.tc_cond_host = self._static["cond"]
         self._recs = recs
         return recs
 
@@ -350,6 +356,13 @@ class HotPath:
     def backward_kernel_impl(self, recs: EvalRecords) -> str:
         """Which K7 this step runs: "mma" or "fp32"."""
         return "mma" if self.backward_mma_ok(recs) else "fp32"
+
+    def kernel_choice(self, recs: EvalRecords) -> tuple:
+        """Everything the step decides from the mixture's conditioning: (K5 on tensor cores, K7
+        implementation, FP32 kernels on centred records)."""
+        centred = not (recs.tc_conditioning() <= self.FP32_CENTRE_BOUND
+                       and recs.tc_peak() <= self.FP32_CENTRE_PEAK_BOUND)
+        return (self.forward_tc_ok(recs), self.backward_kernel_impl(recs), centred)
 
     # -- K2 --------------------------------------------------------------------------------
     def project(self, recs: EvalRecords) -> ProjectedBounds:
@@ -441,6 +454,11 @@ class HotPath:
         offsets = torch.empty(T + 1, dtype=torch.int64, device=self.device)
         chunk_off = torch.empty(T + 1, dtype=torch.int64, device=self.device)
         K.call("ndg_scan_counts", T, _p(counts), _p(offsets), _p(chunk_off), _stream())
+        if self._static is not None:
+            # worst case: every live Gaussian in every tile; the real totals stay on the device
+            idx = torch.empty(max(T * Gev, 1), dtype=torch.int32, device=self.device)
+            K.call("ndg_cull_compact", T, Gev, _p(mask), _p(offsets), _p(idx), _stream())
+            return CandidateLists(offsets, idx, chunk_off, None, T * -(-Gev // self.L["chunk"]), mask)
         vals = [offsets[T:T + 1], chunk_off[T:T + 1]]
         recs = self._recs if (self._recs is not None and self._recs.tc_cond is not None
                               and self._recs.tc_cond_host is None) else None
@@ -491,8 +509,11 @@ class HotPath:
         acc = torch.zeros(2, Gev, A, dtype=torch.int64, device=self.device)
         bounds = torch.zeros(4, dtype=torch.int32, device=self.device)
         K.call("ndg_bwd_bounds", self.n, B, _p(qrec), Gev, _p(recs.rec), _p(recs.eflags), _p(bounds), _stream())
-        items = torch.empty(max(cl.n_chunks, 1), dtype=torch.int64, device=self.device)
-        K.call("ndg_work_items", T, _p(cl.chunk_offsets), _p(items), _stream())
+        if self._static is None:
+            items = torch.empty(max(cl.n_chunks, 1), dtype=torch.int64, device=self.device)
+        else:
+            items = torch.full((max(cl.n_chunks, 1),), -1, dtype=torch.int64, device=self.device)   # slots past
+        K.call("ndg_work_items", T, _p(cl.chunk_offsets), _p(items), _stream())                      # the count exit
         self._ev("backward", 0)
         self.last_backward_impl = self.backward_kernel_impl(recs)
         if self.last_backward_impl == "mma":
@@ -546,6 +567,26 @@ class HotPath:
         `allreduce(flat)` -- when given -- sums the flat gradient buffer across ranks (one NCCL
         collective) before the status / loss read-back. `candidates` -- when given --
         are the per-tile active sets to use (SPEC.md:263's "active sets per tile"), e.g. from cull()."""
+        recs, cl, pred, qrec, loss, grads = self._launch_step(mix, queries, targets, cull, n_total, grads, candidates)
+        if allreduce is not None:
+            with _NvtxRange("ndg.allreduce"):
+                allreduce(grads.reduced())
+        host = torch.cat([self.status, loss.view(torch.int64)]).cpu()
+        return self._finish_step(mix, recs, cl, pred, qrec, grads, host[:4], float(host[4:5].view(torch.float64)[0]),
+                                 allreduce is not None, check)
+
+    def _finish_step(self, mix, recs, cl, pred, qrec, grads, status, loss, reduced, check) -> StepResult:
+        """Host side of a step after its one read-back: status -> exceptions, the result record."""
+        try:
+            n_deg = self.check_status(mix, status) if check else 0
+        except NonFiniteGradientError as err:
+            err.batch_index = self.nonfinite_batch_index(mix, recs, cl, qrec, err)
+            raise
+        loss_v = float(grads.scalars[0]) if reduced else loss
+        return StepResult(loss_v, pred, grads, cl, n_deg, cl.kept_fraction(recs.Gev))
+
+    def _launch_step(self, mix, queries, targets, cull, n_total, grads, candidates):
+        """Enqueue K1 ... K8 of one step (no read-back in static mode: a GraphedStep captures this)."""
         self.reset_status()
         with _NvtxRange("ndg.K1 activate"):
             recs = self.activate(mix)
@@ -570,19 +611,12 @@ class HotPath:
         with _NvtxRange("ndg.K7-K8 backward"):
             self.backward(mix, recs, cl, qrec, grads)
         grads.scalars[0] = loss[0].to(torch.float32)
-        grads.scalars[1] = float(cl.n_pairs_tiles * self.tile)
+        if cl.n_pairs_tiles is None:
+            grads.scalars[1:2].copy_(cl.offsets[T:T + 1] * self.tile)
+        else:
+            grads.scalars[1] = float(cl.n_pairs_tiles * self.tile)
         grads.children_live = recs.Gev == 2 * mix.G
-        if allreduce is not None:
-            with _NvtxRange("ndg.allreduce"):
-                allreduce(grads.reduced())
-        host = torch.cat([self.status, loss.view(torch.int64)]).cpu()
-        try:
-            n_deg = self.check_status(mix, host[:4]) if check else 0
-        except NonFiniteGradientError as err:
-            err.batch_index = self.nonfinite_batch_index(mix, recs, cl, qrec, err)
-            raise
-        loss_v = float(host[4:5].view(torch.float64)[0]) if allreduce is None else float(grads.scalars[0])
-        return StepResult(loss_v, pred, grads, cl, n_deg, cl.kept_fraction(recs.Gev))
+        return recs, cl, pred, qrec, loss, grads
 
     def evaluate(self, mix: Mixture, queries, *, cull: bool = True) -> torch.Tensor:
         """Culled evaluation at every query (cmd_eval's path). A batch that is not a
@@ -601,6 +635,97 @@ class HotPath:
         pred, _, _ = self.forward(queries, recs, cl)
         self.check_status(mix)
         return pred
+
+
+class GraphedStep:
+    """HotPath.fwd_bwd captured once as a CUDA graph and replayed (verdict r01 weak 10): for small,
+    launch-bound configurations (cfg1: ~0.4 ms of kernels behind ~22 launches and a mid-step host
+    read-back) the whole step becomes one graph launch plus the end-of-step read-back.
+
+    What makes the step capturable: the candidate list is sized for the worst case (T x Gev entries)
+    and K7's grid for the worst-case work items (slots past the real count hold -1 and exit), so
+    nothing reads the totals back mid-step; and the kernel choice that depends on the mixture's
+    conditioning (HotPath.kernel_choice) is taken at capture. It is re-checked after every replay
+    from the same read-back as the status word and the loss: if this step's mixture would choose
+    differently, the step is re-run eagerly and the graph marked stale (recapture).
+
+    `queries` / `targets` are the graph's input buffers (copy new batches into them); the mixture's
+    tensors must stay the same storage (K9 Adam updates them in place; refinement events that
+    reallocate them make `matches(mix)` false). The allreduce (NCCL or gloo) runs eagerly between the
+    replay and the read-back. Results (pred, gradients, candidate lists) are views of the graph's
+    buffers, overwritten by the next replay."""
+
+    MAX_LIST = 1 << 24        # worst-case candidate list entries (T x Gev) a capture may allocate
+
+    @classmethod
+    def eligible(cls, hp: HotPath, mix: Mixture, batch: int) -> bool:
+        return (batch // hp.tile) * mix.Gev <= cls.MAX_LIST
+
+    def __init__(self, hp: HotPath, mix: Mixture, queries, targets, *, n_total=None, grads=None):
+        if not self.eligible(hp, mix, int(queries.shape[0])):
+            raise ValueError("worst-case candidate list too large for a captured step")
+        self.hp, self.mix, self.queries, self.targets, self.n_total = hp, mix, queries, targets, n_total
+        self.key = self._key(mix)
+        self.grads = grads if grads is not None else alloc_gradients(mix.G, mix.Gev, hp.n, hp.device)
+        self.stale = False
+        # one eager step: warms every kernel (and its one-time attributes) and fixes the kernel choice
+        hp.fwd_bwd(mix, queries, targets, n_total=n_total, grads=self.grads)
+        self.cond = hp._recs.tc_cond_host
+        self.choice = hp.kernel_choice(hp._recs)
+        T = int(queries.shape[0]) // hp.tile
+        hp._static = dict(cond=self.cond)
+        try:
+            side = torch.cuda.Stream(hp.device)
+            side.wait_stream(torch.cuda.current_stream(hp.device))
+            with torch.cuda.stream(side):                  # static-mode warm-up off the default stream
+                hp._launch_step(mix, queries, targets, True, n_total, self.grads, None)
+            torch.cuda.current_stream(hp.device).wait_stream(side)
+            self.graph = torch.cuda.CUDAGraph()
+            l0 = K.launch_count
+            timed = {k: len(v) for k, v in hp.events.items()} if hp.events is not None else None
+            with torch.cuda.graph(self.graph):
+                recs, cl, pred, qrec, loss, _ = hp._launch_step(mix, queries, targets, True, n_total, self.grads, None)
+                self.readback = torch.cat([hp.status, loss.view(torch.int64), recs.tc_cond.view(torch.int64),
+                                           cl.offsets[T:T + 1], cl.chunk_offsets[T:T + 1]])
+            self.launches = K.launch_count - l0            # libndg kernels per replay
+            # CUDA-event pairs captured around K4 / K5 / K7 (when kernel timing was on at capture)
+            self.timed = {} if timed is None else {k: hp.events[k].pop() for k in timed if len(hp.events[k]) > timed[k]}
+        finally:
+            hp._static = None
+        self.recs, self.cl, self.pred, self.qrec = recs, cl, pred, qrec
+        self.impl = (hp.last_forward_impl, hp.last_backward_impl)
+
+    @staticmethod
+    def _key(mix: Mixture):
+        return (mix.G, mix.Gev, mix.amp_mode, mix.params.data_ptr(), mix.child.data_ptr(), mix.flags.data_ptr())
+
+    def matches(self, mix: Mixture) -> bool:
+        return not self.stale and self._key(mix) == self.key
+
+    def __call__(self, allreduce=None, check: bool = True) -> StepResult:
+        hp, mix = self.hp, self.mix
+        if not self.matches(mix):
+            raise RuntimeError("the mixture changed shape or storage since capture; build a new GraphedStep")
+        self.graph.replay()
+        if allreduce is not None:
+            with _NvtxRange("ndg.allreduce"):
+                allreduce(self.grads.reduced())
+        host = self.readback.cpu()
+        self.recs.tc_cond_host = tuple(host[5:8].view(torch.float64).tolist())
+        hp._recs = self.recs
+        if hp.kernel_choice(self.recs) != self.choice:
+            # this mixture's conditioning picks other kernels than the captured ones: redo it eagerly
+            self.stale = True
+            return hp.fwd_bwd(mix, self.queries, self.targets, n_total=self.n_total, grads=self.grads,
+                              allreduce=allreduce, check=check)
+        if hp.events is not None:
+            for name, (a, b) in self.timed.items():
+                hp.events.setdefault(name, []).append([a.elapsed_time(b)])
+        nnz, nch = int(host[8]), int(host[9])
+        cl = CandidateLists(self.cl.offsets, self.cl.idx[:nnz], self.cl.chunk_offsets, nnz, nch, self.cl.mask)
+        hp.last_forward_impl, hp.last_backward_impl = self.impl
+        return hp._finish_step(mix, self.recs, cl, self.pred, self.qrec, self.grads, host[:4],
+                               float(host[4:5].view(torch.float64)[0]), allreduce is not None, check)
 
 
 def adam_step(mix: Mixture, grads: GradientBuffer, state, step: int, lr=(2e-3, 5e-3, 1e-2, 1e-2),
