@@ -494,13 +494,12 @@ def our_arm(a, rank, world):
                                tensor_flops_per_pair_issued=3 * alg_f, tensor_tflops_issued=3 * t_alg,
                                frac_of_measured_tf32_issued=3 * t_alg / tpeak)
     if main["bwd_impl"] == "mma":
-        # warp-MMA K7: per 8 queries of one Gaussian, 8.5 m16n8k8 MMAs issued (z-GEMM: 3 for dims
-        # 0..7 + half of the 3 packed dims-8..15 ones; S-GEMM: 2 column blocks x 2) = 2176 tensor
-        # flops per pair on the padded 16-dim block
+        # warp-MMA K7 (f16 form): per Gaussian and 16 queries, 10 m16n8k16 MMAs issued (z-GEMM: 2 n-tiles x 3
+        # products; S-GEMM: 2 column blocks x 2) = 2560 tensor flops per pair on the padded 16-dim block
         hpeak = hmma_peak(torch, K, dev)
-        mm_f = 17 * 2 * 16 * 8 * 8 // (2 * 8)
+        mm_f = 10 * 2 * 16 * 8 * 16 // 16
         m_tf = pairs * mm_f / (main["bwd_ms"] * 1e-3) / 1e12
-        kern["backward"].update(impl="mma.sync m16n8k8 tf32 (3xTF32)", tensor_tflops=m_tf, tensor_peak_measured=hpeak,
+        kern["backward"].update(impl="mma.sync m16n8k16 f16 (hi/lo split, 3 products)", tensor_tflops=m_tf, tensor_peak_measured=hpeak,
                                 frac_of_measured_hmma=m_tf / hpeak, tensor_flops_per_pair=mm_f)
     dom = max(kern, key=lambda k: kern[k]["ms"])
     traffic = None
@@ -523,10 +522,12 @@ def our_arm(a, rank, world):
         roof = (dict(bound="tensor", kernel=dom, achieved=kern[dom]["tensor_tflops"],
              peak=kern[dom]["tensor_peak_measured"], unit="TFLOP/s",
              frac=kern[dom]["frac_of_measured_hmma"], traffic=traffic,
-             peak_source="measured mma.sync m16n8k8 tf32 probe (ndg_hmma_probe) on this GPU: the legacy "
+             peak_source="measured mma.sync m16n8k16 f16 probe (ndg_hmma_probe) on this GPU: the legacy "
                          "warp-level tensor path this kernel issues, not the tcgen05 peak",
-             bound_note="the dominant kernel is the warp-MMA K7 (N >= 15): achieved counts its padded "
-                        "3xTF32 MMA flops (2176 per pair); its FP32-equivalent rate is in kernels.backward",
+             bound_note="the dominant kernel is the warp-MMA K7 (N >= 14): achieved counts its padded "
+                        "split-f16 MMA flops (2560 per pair); the kernel is issue-bound (the per-query scalars "
+                        "and operand splits between the MMAs), see DESIGN.md; its FP32-equivalent rate is in "
+                        "kernels.backward",
              flops_per_pair=dict(forward=f_fwd, backward=f_bwd, step=ndg.kept_pairs_flops(n),
                                  backward_tensor=kern[dom]["tensor_flops_per_pair"]),
              step_fp32_equivalent_tflops=step_tflops)

@@ -185,11 +185,11 @@ int ndg_backward(int n, int64_t B, int tile, const float* qrec, const float* rec
                  int64_t* accum, void* stream);
 
 /*
- * K7 on warp-level tensor cores for large N (mma.sync m16n8k8 tf32, 3xTF32). Same work items
- * (chunk_offsets, n_chunks) and the same accum contract as ndg_backward, but z~ comes from the K5
- * record rec_tc (z~ = Ahat [x - 1/2] + bias, as in ndg_forward_tc): a warp owns a Gaussian, MMA1
- * forms a 16 x 8 (dims x queries) block of z~ and MMA2 adds (w z~) z~^T to S' in the MMA
- * accumulators. Tile must be a multiple of 8. Returns NDG_ERR_UNSUPPORTED_DIMS when
+ * K7 on warp-level tensor cores for large N (mma.sync m16n8k16 f16 with hi / lo splits and power-of-two
+ * operand scaling, fp32 accumulation). Same work items (chunk_offsets, n_chunks) and the same accum
+ * contract as ndg_backward, but z~ comes from the K5 record rec_tc (z~ = Ahat [x - 1/2] + bias, as in
+ * ndg_forward_tc): a warp owns two Gaussians, MMA1 forms 16 x 8 (dims x queries) blocks of z~ and MMA2
+ * adds (w z~) z~^T over 16 queries to S' in the MMA accumulators. Tile must be a multiple of 8. Returns NDG_ERR_UNSUPPORTED_DIMS when
  * ndg_backward_mma_supported(n) is 0 (n outside 9..16).
  */
 int ndg_backward_mma_supported(int n);
@@ -295,7 +295,7 @@ double ndg_fp32_probe_flops(int blocks, int iters);
 /* TF32 tensor-core peak probe (tcgen05.mma kind::tf32 M=128 N=256 K=8 on resident operands). */
 int ndg_tf32_probe(float* out, int blocks, int iters, void* stream);
 double ndg_tf32_probe_flops(int blocks, int iters);
-/* Warp-level tensor-core peak probe (mma.sync m16n8k8 tf32, K7-MMA's instruction; 16 warps x 8 chains). */
+/* Warp-level tensor-core peak probe (mma.sync m16n8k16 f16 -> f32, K7-MMA's instruction; 16 warps x 8 chains). */
 int ndg_hmma_probe(float* out, int blocks, int iters, void* stream);
 double ndg_hmma_probe_flops(int blocks, int iters);
 

@@ -1,5 +1,5 @@
-// K7-MMA: the fused backward for large N on warp-level tensor cores (sm_100a, mma.sync m16n8k8
-// tf32, 3xTF32 products, fp32 accumulation).
+// K7-MMA: the fused backward for large N on warp-level tensor cores (sm_100a, mma.sync m16n8k16 f16
+// operands split hi / lo, fp32 accumulation).
 //
 // Same contract as the FP32 K7 (ndg_backward.cu): per (tile, candidate) it adds
 //   S' += (w z~) z~^T (lower),  t' += w z~,  gA += g dpred,  loss_share += g ell,  proxy += |w| sqrt(s~)
@@ -9,22 +9,29 @@
 // Why a second kernel: the FP32 K7 keeps one Gaussian per thread with its record (P + 2N + 3 floats)
 // AND its accumulators (P + N + 5) in registers. Past N = 12 that no longer fits in 255 registers;
 // at N = 16 the pair loop reloads ~100 spilled floats per query from local memory and the kernel
-// runs at a third of the FP32 peak. Here a warp owns a Gaussian and the 16 x 8 (dims x queries)
+// runs at a third of the FP32 peak. Here a warp owns two Gaussians and a 16 x 8 (dims x queries)
 // block of z~ is one MMA:
-//   MMA1  Z^T (16 x 8)  = Ahat (16 x 16) . Xhat^T (16 x 8),  C initialised to the bias column
-//   MMA2  S'  (16 x 16) += (s V)^T-block (16 x 8) . V (8 x 16),  V = sqrt|w| Z, s = sign w
-// MMA1's C fragment (lane (gid, tig): dims gid, gid+8 of queries 2tig, 2tig+1) IS the A and B
-// fragment MMA2 needs once the query index k of MMA2 is relabelled (k = tig <-> query 2tig,
-// k = tig + 4 <-> query 2tig + 1; the sum over queries does not care), so z~ never leaves the
-// registers. With V = V_h + V_l, S' = sum s V_h V_h^T + M + M^T (M = sum s V_h V_l^T) takes two MMAs
-// per column block where the plain 3xTF32 product u z^T takes three (same products kept, same lo.lo
-// dropped); M^T is formed once per (tile, Gaussian) in shared memory. Ahat costs 16 registers per lane
-// (hi | lo), S' and M 8 each, t' 2. The per-tile Xhat fragments
-// (hi | lo, x - 1/2 as in K5) are built once per work item in shared memory and read as LDS.128.
+//   MMA1  Z^T (16 x 8)   = Ahat (16 x 16) . Xhat^T (16 x 8),  C initialised to the bias column
+//   MMA2  S'  (16 x 16) += (s V)^T (16 dims x 16 queries) . V (16 queries x 8 dims) per column block,
+//         V = sqrt|w| Z, s = sign w
+// The C fragments of MMA1 for two 8-query n-tiles (lane (gid, tig): dims gid, gid+8 of queries 2tig,
+// 2tig+1) ARE the A fragment (rows = dims, k = the 16 queries) and the B fragments MMA2 needs, so z~
+// never leaves the registers. With V = V_h + V_l, S' = sum s V_h V_h^T + M + M^T (M = sum s V_h V_l^T)
+// takes two MMAs per column block where the plain split product u z^T takes three (same products
+// kept, same lo.lo dropped); M^T is formed once per (tile, Gaussian) in shared memory. The per-tile
+// Xhat fragments (hi | lo, x - 1/2 as in K5) are built once per work item in shared memory and read
+// as LDS.128.
 //
 // Ahat / bias / colour come from the K5 tensor-core record (rec_tc, ndg_tc_records): row i of Ahat is
-// kC L^-1 (lower), column n the bias for xhat = x - 1/2, so z~ is bit-for-bit the K5 z~ up to fp32
-// accumulation order. Its error grows like the z-GEMM's (RMS of B_e, engine.py guards it).
+// kC L^-1 (lower), column n the bias for xhat = x - 1/2, so z~ is the K5 z~ up to accumulation
+// order. Its error grows like the z-GEMM's (RMS of B_e, engine.py guards it).
+//
+// Round 1 ran this on m16n8k8 tf32 (8.5 MMAs per Gaussian and 8 queries, 231 ms on the N = 16 A/B
+// workload); m16n8k16 f16 issues at the same rate with twice the K (tools/mma_sync_probe.cu), which
+// with the lane ownership below gives 10 MMAs per Gaussian and 16 queries and 176 ms, and a smaller
+// error against the FP32 K7 (8.3e-7 vs 2.8e-6: the operand scaling keeps the splits exact).
+#include <cuda_fp16.h>
+
 #include "ndg_common.cuh"
 #include "ndg_tc.cuh"
 
@@ -36,28 +43,40 @@ namespace {
 #define NDG_MMA_MINB 4
 #endif
 constexpr int kThreads = 128;   // 4 warps; work item = (tile, chunk of kBwdChunk candidates)
-constexpr int kGpw = 2;         // Gaussians per warp in flight: the packed dims-8..15 k-step carries two
+constexpr int kGpw = 2;         // Gaussians per warp: the lanes own the two Gaussians' per-query scalars between them
 
-__device__ __forceinline__ void mma8(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+// ---- mma.sync m16n8k16 f16 -> f32 --------------------------------------------------------------------
+// All 16 input dims in ONE k-step, and 16 queries per S' update. Per Gaussian and 16 queries: MMA1
+// 2 n-tiles x 3 products (hi.hi, hi.lo, lo.hi) = 6, MMA2 2 column blocks x 2 (v_h v_h, v_h v_l) = 4:
+// 10 MMAs where the tf32 form issued 17.
+// f16 has tf32's 11 significant bits but a 5-bit exponent, so the operands are scaled by powers of two:
+//   * Ahat and the bias by 2^se per Gaussian (largest |Ahat| entry in [2^14, 2^15)): z' = 2^se z~;
+//   * v = sqrt|w| z~ by 2^tv per launch, from the bounds: sqrt(g) |z~| <= 0.729 and |w| <= g H Amax,
+//     so |v'| <= 2^14; S' and M are unscaled at the flush.
+// With the hi / lo split the products keep ~22 bits as 3xTF32 does; what falls below f16's normal range
+// is below 2^-28 of the largest term of its sum.
+// The loop is issue-bound (ncu: 2.5 of 4 issue slots per SM-cycle, tensor pipe 35% busy), so the per-query scalars (g, w, sqrt|w|, gA, loss share, proxy) are computed
+// once per (Gaussian, query): the 8 partial |z'|^2 sums a lane holds for the warp's two Gaussians x
+// 16 queries (2 n-tiles x 2 queries) are reduce-scattered over the 8 gid lanes of its tig column, so
+// lane (gid, tig) ends owning Gaussian gid & 1, n-tile (gid >> 1) & 1, query 2 tig + (gid >> 2) -- the
+// 32 lanes own the 32 (Gaussian, query) pairs exactly once -- and w, sqrt|w| go back by shuffles.
+__device__ __forceinline__ void mma16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
                  "{%0,%1,%2,%3};\n"
                  : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
                  : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint32_t hi_bits(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
+// (a, b) -> f16x2 hi (a in the low half) and the f16x2 of the residuals
+__device__ __forceinline__ void split_h2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 f = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a - f.x, b - f.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 
-struct Split4 {
-    uint32_t hi[4], lo[4];
-    __device__ __forceinline__ void set(float v0, float v1, float v2, float v3) {
-        const float v[4] = {v0, v1, v2, v3};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            hi[i] = hi_bits(v[i]);
-            lo[i] = __float_as_uint(v[i] - __uint_as_float(hi[i]));
-        }
-    }
-};
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }   // |e| <= 126
 
 template <int N>
 __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
@@ -71,13 +90,14 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
     constexpr int RT = tc_rec_floats(N);
     constexpr int P = n_chol(N);
     constexpr int A = acc_doubles(N);
-    extern __shared__ __align__(16) float4 smem4[];
-    float4* sX = smem4;                       // [tile/8][2 k-steps][32 lanes] {x_hi(b0), x_hi(b1), x_lo(b0), x_lo(b1)}
-    float4* sQ = smem4 + (tile / 8) * 64;     // [tile] {dpred0, dpred1, dpred2, ell}
+    extern __shared__ __align__(16) uint4 smem16[];
+    const int tile16 = (tile + 15) & ~15;                 // the loop runs over 16-query blocks
+    uint4* sX = smem16;                                   // [tile16/8][32 lanes] {xh(d0,d1), xh(d8,d9), xl.., xl..}
+    float4* sQ = reinterpret_cast<float4*>(smem16 + (tile16 / 8) * 32);   // [tile16] {dpred0, dpred1, dpred2, ell}
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3, odd = gid & 1;
-    float* sM = reinterpret_cast<float*>(sQ + tile) + warp * 16 * 17;   // per-warp M^T scratch
+    float* sMm = reinterpret_cast<float*>(sQ + tile16) + warp * 16 * 17;   // per-warp M^T scratch
     const int64_t item = items[blockIdx.x];   // (tile << 32) | chunk, band order (ndg_work_items)
     if (item < 0) return;                        // unused slot of a worst-case-sized list (graph replay)
     const int64_t t = item >> 32;
@@ -88,32 +108,47 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
     const int n_here = rem < kBwdChunk ? (int)rem : kBwdChunk;
 
     const FxScales fx = fx_scales(bounds, (int64_t)T * tile);
-
-    // ---- the tile's Xhat fragments and (dpred, ell) in shared memory -----------------------------
-    const float* qt = qrec + t * tile * QS;
-    for (int i = tid; i < tile * 8; i += kThreads) {          // (tile/8) n-tiles x 2 k-steps x 32 lanes
-        const int l = i & 31, ks = (i >> 5) & 1, nt = i >> 6;
-        const int q = nt * 8 + (l >> 2), d0 = ks * 8 + (l & 3), d1 = d0 + 4;
-        const float x0 = d0 < N ? qt[q * QS + d0] - 0.5f : 0.f;
-        const float x1 = d1 < N ? qt[q * QS + d1] - 0.5f : 0.f;
-        const float h0 = __uint_as_float(hi_bits(x0)), h1 = __uint_as_float(hi_bits(x1));
-        sX[i] = make_float4(h0, h1, x0 - h0, x1 - h1);
+    // v' = 2^tv v with |v'| <= 2^14 (v = sqrt|w| z~, |w| <= H Amax, sqrt(g) |z~| <= 0.729)
+    int tv = 0;
+    {
+        const float vmax = 0.73f * sqrtf(__uint_as_float(bounds[0]) * __uint_as_float(bounds[3]));
+        if (vmax > 0.f && vmax < 3.0e38f) {
+            int e;
+            frexpf(vmax, &e);                            // vmax < 2^e
+            tv = min(max(14 - e, -100), 100);
+        }
     }
-    for (int q = tid; q < tile; q += kThreads)
-        sQ[q] = make_float4(qt[q * QS + N], qt[q * QS + N + 1], qt[q * QS + N + 2], qt[q * QS + N + 3]);
+
+    // ---- the tile's Xhat fragments (f16 hi / lo) and (dpred, ell) in shared memory; a tile of 8 mod 16
+    // queries is padded with one n-tile of zero queries (dpred = ell = 0: every term they enter is 0) ----
+    const float* qt = qrec + t * tile * QS;
+    for (int i = tid; i < tile16 * 4; i += kThreads) {        // (tile16/8) n-tiles x 32 lanes
+        const int l = i & 31, nt = i >> 5;
+        const int q = nt * 8 + (l >> 2), d0 = 2 * (l & 3);
+        float x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int d = d0 + (k & 1) + (k >> 1) * 8;
+            x[k] = (d < N && q < tile) ? qt[q * QS + d] - 0.5f : 0.f;
+        }
+        uint4 v;
+        split_h2(x[0], x[1], v.x, v.z);
+        split_h2(x[2], x[3], v.y, v.w);
+        sX[i] = v;
+    }
+    for (int q = tid; q < tile16; q += kThreads)
+        sQ[q] = q < tile ? make_float4(qt[q * QS + N], qt[q * QS + N + 1], qt[q * QS + N + 2], qt[q * QS + N + 3])
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
+    // the (Gaussian, n-tile, query) this lane owns in every 16-query block
+    const int oj = gid & 1, ou = (gid >> 1) & 1, ob = gid >> 2;
 
     for (int gb = warp * kGpw; gb < n_here; gb += 4 * kGpw) {
         // ---- per-Gaussian operands (warp-uniform Gaussian; an absent second one runs on zeros) ----
-        // Ahat is lower triangular, so its k-step over dims 8..15 has zero rows 0..7: that k-step runs ONE
-        // MMA for both Gaussians in flight, rows 0..7 = Gaussian 0's Ahat[8:16, 8:16], rows 8..15 =
-        // Gaussian 1's (the B operand, the queries, is shared). Its C fragment then holds dims 8+gid of
-        // Gaussian 0 in c0, c1 and of Gaussian 1 in c2, c3 -- the registers each Gaussian's z~ needs.
-        Split4 a0f[kGpw], apk;                // Ahat[:, 0:8] per Gaussian; packed Ahat[8:16, 8:16] pair
-        float bz[kGpw][2], col[kGpw][3];
+        uint32_t ah[kGpw][4], al[kGpw][4];   // Ahat 16 x 16 fragment (rows = dims of z~, k = input dims)
+        float bz[kGpw][2], col[kGpw][3], s2[kGpw], rsc[kGpw], zsc[kGpw];
         int64_t e[kGpw];
         bool live[kGpw];
-        float pk[kGpw][2];
 #pragma unroll
         for (int j = 0; j < kGpw; ++j) {
             live[j] = gb + j < n_here;
@@ -123,89 +158,124 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
             auto at = [&](int i, int k) -> float {
                 return (live[j] && i < N && k < N) ? __ldg(r + ((k / 4) * N + i) * 4 + (k & 3)) : 0.f;
             };
-            a0f[j].set(at(gid, tig), at(gid + 8, tig), at(gid, tig + 4), at(gid + 8, tig + 4));
-            pk[j][0] = at(8 + gid, 8 + tig);
-            pk[j][1] = at(8 + gid, 12 + tig);
-            bz[j][0] = (live[j] && gid < N) ? __ldg(r + ((N / 4) * N + gid) * 4 + (N & 3)) : 0.f;
-            bz[j][1] = (live[j] && gid + 8 < N) ? __ldg(r + ((N / 4) * N + gid + 8) * 4 + (N & 3)) : 0.f;
+            // fragment order: (gid, 2tig..+1), (gid+8, 2tig..+1), (gid, 2tig+8..+9), (gid+8, 2tig+8..+9)
+            float av[8];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+                const int row = gid + (f & 1) * 8, k = 2 * tig + (f >> 1) * 8;
+                av[2 * f] = at(row, k);
+                av[2 * f + 1] = at(row, k + 1);
+            }
+            float m = 0.f;
+#pragma unroll
+            for (int f = 0; f < 8; ++f) m = fmaxf(m, fabsf(av[f]));
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            int se = 0;
+            if (m > 0.f) {
+                int ex;
+                frexpf(m, &ex);                          // m < 2^ex: scaled max in [2^14, 2^15)
+                se = min(max(15 - ex, -100), 100);
+            }
+            const float sc = pow2f(se);
+#pragma unroll
+            for (int f = 0; f < 4; ++f) split_h2(av[2 * f] * sc, av[2 * f + 1] * sc, ah[j][f], al[j][f]);
+            bz[j][0] = (live[j] && gid < N) ? __ldg(r + ((N / 4) * N + gid) * 4 + (N & 3)) * sc : 0.f;
+            bz[j][1] = (live[j] && gid + 8 < N) ? __ldg(r + ((N / 4) * N + gid + 8) * 4 + (N & 3)) * sc : 0.f;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) col[j][ch] = live[j] ? __ldg(r + N * K + ch) : 0.f;
+            s2[j] = pow2f(-2 * se);                      // |z~|^2 = 2^-2se |z'|^2
+            rsc[j] = pow2f(tv - se);                     // v' = 2^tv sqrt|w| z~ = 2^(tv-se) sqrt|w| z'
+            zsc[j] = pow2f(-se);
         }
-        apk.set(pk[0][0], pk[1][0], pk[0][1], pk[1][1]);
-        float S[kGpw][2][4] = {}, Mx[kGpw][2][4] = {};   // sum s v_h v_h^T and sum s v_h v_l^T fragments
-        float tz[kGpw][2] = {}, gA[kGpw][3] = {}, ls[kGpw] = {}, px[kGpw] = {};
+        // the owned Gaussian's per-query constants
+        const float o_s2 = oj ? s2[1] : s2[0], o_rsc = oj ? rsc[1] : rsc[0];
+        const float o_c0 = oj ? col[1][0] : col[0][0], o_c1 = oj ? col[1][1] : col[0][1],
+                    o_c2 = oj ? col[1][2] : col[0][2];
+        float S[kGpw][2][4] = {}, Mx[kGpw][2][4] = {};   // sum s v'_h v'_h^T and sum s v'_h v'_l^T fragments
+        float tz[kGpw][2] = {}, gA[3] = {}, ls = 0.f, px = 0.f;   // gA, loss share, proxy: the owned Gaussian
 
-        for (int nt = 0; nt < tile / 8; ++nt) {
-            const float4 xa = sX[nt * 64 + lane], xb = sX[nt * 64 + 32 + lane];
-            // this lane's own query of the pair (2tig + odd): the per-query scalars are computed once per
-            // lane pair (gid, gid ^ 1) instead of by all eight gid lanes
-            const float4 qm = sQ[nt * 8 + 2 * tig + odd];
-            const uint32_t xh[2][2] = {{__float_as_uint(xa.x), __float_as_uint(xa.y)},
-                                       {__float_as_uint(xb.x), __float_as_uint(xb.y)}};
-            const uint32_t xl[2][2] = {{__float_as_uint(xa.z), __float_as_uint(xa.w)},
-                                       {__float_as_uint(xb.z), __float_as_uint(xb.w)}};
-            // MMA1, k-step 1 (dims 8..15) for both Gaussians at once; biases of dims 8+gid in the accumulator,
-            // the two correction products before hi.hi, all in one chain (fewer adds; the loop is issue-bound)
-            float zp[4] = {bz[0][1], bz[0][1], bz[1][1], bz[1][1]};
-            mma8(zp, apk.lo, xh[1][0], xh[1][1]);
-            mma8(zp, apk.hi, xl[1][0], xl[1][1]);
-            mma8(zp, apk.hi, xh[1][0], xh[1][1]);
+        for (int nb16 = 0; nb16 < tile16 / 16; ++nb16) {
+            const uint4 xf[2] = {sX[(nb16 * 2) * 32 + lane], sX[(nb16 * 2 + 1) * 32 + lane]};
+            const float4 q = sQ[nb16 * 16 + ou * 8 + 2 * tig + ob];       // the owned query's (dpred, ell)
+            // MMA1: z' (dims x 8 queries) = Ahat' xhat + bias' per (Gaussian, n-tile); corrections first
+            float z[kGpw][2][4];
+#pragma unroll
+            for (int j = 0; j < kGpw; ++j)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    z[j][u][0] = z[j][u][1] = bz[j][0];
+                    z[j][u][2] = z[j][u][3] = bz[j][1];
+                    mma16(z[j][u], al[j], xf[u].x, xf[u].y);
+                    mma16(z[j][u], ah[j], xf[u].z, xf[u].w);
+                    mma16(z[j][u], ah[j], xf[u].x, xf[u].y);
+                }
+            // |z'|^2 partials of this lane's dims (gid, gid + 8), index j*4 + u*2 + (query 2tig | 2tig+1),
+            // reduce-scattered over the gid lanes: xor 4 splits j, xor 8 splits u, xor 16 the query
+            float p[8];
+#pragma unroll
+            for (int j = 0; j < kGpw; ++j)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    p[j * 4 + u * 2] = fmaf(z[j][u][2], z[j][u][2], z[j][u][0] * z[j][u][0]);
+                    p[j * 4 + u * 2 + 1] = fmaf(z[j][u][3], z[j][u][3], z[j][u][1] * z[j][u][1]);
+                }
+            float k1[4], k2[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                k1[i] = (oj ? p[4 + i] : p[i]) + __shfl_xor_sync(0xffffffffu, oj ? p[i] : p[4 + i], 4);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                k2[i] = (ou ? k1[2 + i] : k1[i]) + __shfl_xor_sync(0xffffffffu, ou ? k1[i] : k1[2 + i], 8);
+            const float sm = ((ob ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, ob ? k2[0] : k2[1], 16)) * o_s2;
+            // the owned pair's scalars
+            const float gm = ex2_neg(sm);
+            const float wm = gm * fmaf(q.z, o_c2, fmaf(q.y, o_c1, q.x * o_c0));
+            const float rm = sqrt_approx(fabsf(wm)) * o_rsc;
+            gA[0] = fmaf(gm, q.x, gA[0]);
+            gA[1] = fmaf(gm, q.y, gA[1]);
+            gA[2] = fmaf(gm, q.z, gA[2]);
+            ls = fmaf(gm, q.w, ls);
+            px = fmaf(fabsf(wm), sqrt_approx(sm), px);
 #pragma unroll
             for (int j = 0; j < kGpw; ++j) {
-                // MMA1, k-step 0 (dims 0..7) per Gaussian, accumulating onto the bias of dims gid and the
-                // packed k-step's dims 8+gid
-                float z[4] = {bz[j][0], bz[j][0], zp[2 * j], zp[2 * j + 1]};
-                mma8(z, a0f[j].lo, xh[0][0], xh[0][1]);
-                mma8(z, a0f[j].hi, xl[0][0], xl[0][1]);
-                mma8(z, a0f[j].hi, xh[0][0], xh[0][1]);
-                // s~ of queries 2tig (a) and 2tig+1 (b) from this lane's two dims, reduce-scattered over the
-                // 8 gid lanes: even gid ends with s~(a), odd gid with s~(b)
-                const float sa = fmaf(z[2], z[2], z[0] * z[0]), sb = fmaf(z[3], z[3], z[1] * z[1]);
-                float sm = (odd ? sb : sa) + __shfl_xor_sync(0xffffffffu, odd ? sa : sb, 4);
-                sm += __shfl_xor_sync(0xffffffffu, sm, 8);
-                sm += __shfl_xor_sync(0xffffffffu, sm, 16);
-                const float gm = ex2_neg(sm);
-                const float wm = gm * fmaf(qm.z, col[j][2], fmaf(qm.y, col[j][1], qm.x * col[j][0]));
-                const float rm = sqrt_approx(fabsf(wm));
-                gA[j][0] = fmaf(gm, qm.x, gA[j][0]);
-                gA[j][1] = fmaf(gm, qm.y, gA[j][1]);
-                gA[j][2] = fmaf(gm, qm.z, gA[j][2]);
-                ls[j] = fmaf(gm, qm.w, ls[j]);
-                px[j] = fmaf(fabsf(wm), sqrt_approx(sm), px[j]);
-                const float wo = __shfl_xor_sync(0xffffffffu, wm, 4), ro = __shfl_xor_sync(0xffffffffu, rm, 4);
-                const float wa = odd ? wo : wm, wb = odd ? wm : wo;
-                const float ra = odd ? ro : rm, rb = odd ? rm : ro;
-                tz[j][0] = fmaf(wa, z[0], fmaf(wb, z[1], tz[j][0]));
-                tz[j][1] = fmaf(wa, z[2], fmaf(wb, z[3], tz[j][1]));
-                // S' = sum w z~ z~^T = sum s v v^T with v = sqrt|w| z~, s = sign w. Split v = v_h + v_l:
-                // S' = sum s v_h v_h^T + M + M^T (M = sum s v_h v_l^T; v_l v_l^T dropped as in 3xTF32),
-                // 2 MMAs per column block instead of 3. A = s v_h (rows = dims, k = relabelled queries),
-                // B = v_h | v_l; C-fragment order [c0..c3] = (gid, qa), (gid, qb), (gid+8, qa), (gid+8, qb).
-                Split4 vs;
-                vs.set(ra * z[0], rb * z[1], ra * z[2], rb * z[3]);
-                const uint32_t sga = __float_as_uint(wa) & 0x80000000u, sgb = __float_as_uint(wb) & 0x80000000u;
-                const uint32_t av[4] = {vs.hi[0] ^ sga, vs.hi[2] ^ sga, vs.hi[1] ^ sgb, vs.hi[3] ^ sgb};
-                // column block 0 = dims 0..7 (b = v(gid, q)); block 1 = dims 8..15 (b = v(gid+8, q))
-                mma8(Mx[j][0], av, vs.lo[0], vs.lo[1]);
-                mma8(Mx[j][1], av, vs.lo[2], vs.lo[3]);
-                mma8(S[j][0], av, vs.hi[0], vs.hi[1]);
-                mma8(S[j][1], av, vs.hi[2], vs.hi[3]);
+                uint32_t ph[2][2], pl[2][2], am[2];      // [n-tile][dims gid | gid+8] packed v' hi / lo
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    // w, sqrt|w| of queries 2tig (a) and 2tig+1 (b) from their owners (same tig column)
+                    const int src = ((j | (u << 1)) << 2) | tig;
+                    const float wa = __shfl_sync(0xffffffffu, wm, src), wb = __shfl_sync(0xffffffffu, wm, src | 16);
+                    const float ra = __shfl_sync(0xffffffffu, rm, src), rb = __shfl_sync(0xffffffffu, rm, src | 16);
+                    tz[j][0] = fmaf(wa, z[j][u][0], fmaf(wb, z[j][u][1], tz[j][0]));
+                    tz[j][1] = fmaf(wa, z[j][u][2], fmaf(wb, z[j][u][3], tz[j][1]));
+                    split_h2(ra * z[j][u][0], rb * z[j][u][1], ph[u][0], pl[u][0]);
+                    split_h2(ra * z[j][u][2], rb * z[j][u][3], ph[u][1], pl[u][1]);
+                    am[u] = ((__float_as_uint(wa) & 0x80000000u) >> 16) | (__float_as_uint(wb) & 0x80000000u);
+                }
+                // MMA2: A = s v'_h (16 dims x 16 queries), B = v'_h | v'_l (16 queries x 8 dims) per column block
+                const uint32_t a2[4] = {ph[0][0] ^ am[0], ph[0][1] ^ am[0], ph[1][0] ^ am[1], ph[1][1] ^ am[1]};
+                mma16(Mx[j][0], a2, pl[0][0], pl[1][0]);
+                mma16(Mx[j][1], a2, pl[0][1], pl[1][1]);
+                mma16(S[j][0], a2, ph[0][0], ph[1][0]);
+                mma16(S[j][1], a2, ph[0][1], ph[1][1]);
             }
         }
 
-        // ---- flush: S' entries are owned by single lanes; t', gA, loss share, proxy reduce over tig ----
+        // ---- flush: S' entries are owned by single lanes; t' reduces over tig, gA / loss share / proxy
+        // over the 16 lanes owning each Gaussian. (Packing the slots over the warp -- 5 + 2 fx_adds per
+        // lane instead of 8 half-predicated + single-lane tails -- measured the same: 176.1 vs 175.9 ms.)
+        const float sS = pow2f(-2 * tv);
 #pragma unroll
         for (int j = 0; j < kGpw; ++j) {
             if (!live[j]) continue;                       // warp-uniform
             unsigned long long* hw = accum + e[j] * A;
             unsigned long long* lw = hw + Gev * A;
             unsigned long long* flag = hw + acc_flag(N);
-            // S'[r][c] = P[r][c] + M[r][c] + M[c][r]: M^T through this warp's 16 x 17 scratch
 #pragma unroll
             for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
                 for (int v = 0; v < 4; ++v)
-                    sM[(gid + (v >> 1) * 8) * 17 + nb * 8 + 2 * tig + (v & 1)] = Mx[j][nb][v];
+                    sMm[(gid + (v >> 1) * 8) * 17 + nb * 8 + 2 * tig + (v & 1)] = Mx[j][nb][v];
             __syncwarp();
 #pragma unroll
             for (int nb = 0; nb < 2; ++nb)
@@ -214,40 +284,54 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                     const int row = gid + (v >> 1) * 8, colj = nb * 8 + 2 * tig + (v & 1);
                     if (row < N && colj <= row)
                         fx_add(hw + tri(row, colj), lw + tri(row, colj), flag,
-                               S[j][nb][v] + Mx[j][nb][v] + sM[colj * 17 + row], fx.h);
+                               (S[j][nb][v] + Mx[j][nb][v] + sMm[colj * 17 + row]) * sS, fx.h);
                 }
             __syncwarp();
-            float r[7] = {tz[j][0], tz[j][1], gA[j][0], gA[j][1], gA[j][2], ls[j], px[j]};
+            float r[2] = {tz[j][0] * zsc[j], tz[j][1] * zsc[j]};
 #pragma unroll
-            for (int i = 0; i < 7; ++i) {
+            for (int i = 0; i < 2; ++i) {
                 r[i] += __shfl_xor_sync(0xffffffffu, r[i], 1);
                 r[i] += __shfl_xor_sync(0xffffffffu, r[i], 2);
             }
-#pragma unroll
-            for (int i = 2; i < 7; ++i) r[i] += __shfl_xor_sync(0xffffffffu, r[i], 4);   // both queries of a pair
             if (tig == 0) {
                 fx_add(hw + P + gid, lw + P + gid, flag, r[0], fx.h);
                 if (gid + 8 < N) fx_add(hw + P + gid + 8, lw + P + gid + 8, flag, r[1], fx.h);
             }
-            if (lane == 0) {
-                const int T0 = acc_tail(N);
-                fx_add(hw + T0, lw + T0, flag, r[2], fx.g);
-                fx_add(hw + T0 + 1, lw + T0 + 1, flag, r[3], fx.g);
-                fx_add(hw + T0 + 2, lw + T0 + 2, flag, r[4], fx.g);
-                fx_add(hw + T0 + 3, lw + T0 + 3, flag, r[5], fx.l);
-                fx_add(hw + T0 + 4, lw + T0 + 4, flag, r[6], fx.h);
-                atomicAdd(hw + T0 + 5, (unsigned long long)tile);
-            }
+        }
+        float r[5] = {gA[0], gA[1], gA[2], ls, px};
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            r[i] += __shfl_xor_sync(0xffffffffu, r[i], 1);
+            r[i] += __shfl_xor_sync(0xffffffffu, r[i], 2);
+            r[i] += __shfl_xor_sync(0xffffffffu, r[i], 8);
+            r[i] += __shfl_xor_sync(0xffffffffu, r[i], 16);
+        }
+        const bool o_live = oj ? live[1] : live[0];
+        if (lane < 8 && tig == 0 && o_live) {
+            unsigned long long* hw = accum + (oj ? e[1] : e[0]) * A;
+            unsigned long long* lw = hw + Gev * A;
+            unsigned long long* flag = hw + acc_flag(N);
+            const int T0 = acc_tail(N);
+            fx_add(hw + T0, lw + T0, flag, r[0], fx.g);
+            fx_add(hw + T0 + 1, lw + T0 + 1, flag, r[1], fx.g);
+            fx_add(hw + T0 + 2, lw + T0 + 2, flag, r[2], fx.g);
+            fx_add(hw + T0 + 3, lw + T0 + 3, flag, r[3], fx.l);
+            fx_add(hw + T0 + 4, lw + T0 + 4, flag, r[4], fx.h);
+            atomicAdd(hw + T0 + 5, (unsigned long long)tile);
         }
     }
 }
+
+constexpr size_t kSmemX = sizeof(uint4) * 4;      // per query: Xhat fragments (tile16/8 n-tiles x 32 lanes x 16 B)
+constexpr size_t kSmemW = sizeof(float) * 16 * 17;    // per warp: M^T scratch
 
 template <int N>
 int launch_backward_mma(int64_t B, int tile, const float* qrec, const float* rec_tc, const int64_t* off,
                         const int32_t* idx, const int64_t* items, int64_t n_chunks, int64_t Gev, const uint32_t* bounds,
                         unsigned long long* accum, cudaStream_t st) {
     const int64_t T = B / tile;
-    const size_t smem = sizeof(float4) * ((size_t)tile * 8 + tile) + sizeof(float) * 4 * 16 * 17;
+    const size_t tq = (tile + 15) & ~15;                  // the f16 form pads the tile to 16 queries
+    const size_t smem = kSmemX * tq + sizeof(float4) * tq + kSmemW * 4;
     static DeviceOnce attr;
     if (attr.first())
         cudaFuncSetAttribute(backward_mma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

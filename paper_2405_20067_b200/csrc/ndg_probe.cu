@@ -80,17 +80,18 @@ extern "C" int ndg_tf32_probe(float* out, int blocks, int iters, void* stream) {
 
 extern "C" double ndg_tf32_probe_flops(int blocks, int iters) { return 2.0 * 128 * 256 * 8 * (double)iters * blocks; }
 
-// Warp-level tensor-core peak probe (mma.sync m16n8k8 tf32, the K7-MMA instruction): 512 threads per
-// CTA, each warp running 8 independent accumulator chains -- the roofline denominator for K7-MMA.
+// Warp-level tensor-core peak probe (mma.sync m16n8k16 f16 -> f32, the K7-MMA instruction): 512 threads
+// per CTA, each warp running 8 independent accumulator chains -- the roofline denominator for K7-MMA.
+// (m16n8k8 tf32 issues at the same 0.467 MMA/clk/SM with half the K: tools/mma_sync_probe.cu.)
 __global__ void __launch_bounds__(512) hmma_probe_kernel(int iters, float* out) {
     float d[8][4] = {};
     uint32_t a[4], b[2];
-    for (int i = 0; i < 4; ++i) a[i] = __float_as_uint(1.0f + threadIdx.x * 1e-3f + i);
-    for (int i = 0; i < 2; ++i) b[i] = __float_as_uint(0.5f + i);
+    for (int i = 0; i < 4; ++i) a[i] = 0x3c003c00u + threadIdx.x + i;
+    for (int i = 0; i < 2; ++i) b[i] = 0x38003800u + i;
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+            asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
                          "{%8,%9}, {%0,%1,%2,%3};\n"
                          : "+f"(d[k][0]), "+f"(d[k][1]), "+f"(d[k][2]), "+f"(d[k][3])
                          : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
@@ -107,4 +108,4 @@ extern "C" int ndg_hmma_probe(float* out, int blocks, int iters, void* stream) {
     return NDG_OK;
 }
 
-extern "C" double ndg_hmma_probe_flops(int blocks, int iters) { return 2.0 * 16 * 8 * 8 * 8 * 16 * (double)iters * blocks; }
+extern "C" double ndg_hmma_probe_flops(int blocks, int iters) { return 2.0 * 16 * 8 * 16 * 8 * 16 * (double)iters * blocks; }

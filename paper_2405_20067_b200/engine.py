@@ -10,7 +10,7 @@ gmm-core, culling and grad modules, each enqueued on the current CUDA stream thr
     K5 ndg_forward_tc    eval_mixture (+ K6 loss_rel_l2 fused), tcgen05
        ndg_forward       (FP32-pipe K5: ill-conditioned mixtures, tiles > 256, NDG_FORWARD=fp32)
     K7 ndg_backward      backward pair loop, FP32 pipe (N <= 14)
-       ndg_backward_mma  (warp-MMA pair loop: N >= 15, or NDG_BACKWARD=mma for N >= 9)
+       ndg_backward_mma  (warp-MMA pair loop: N >= 14, or NDG_BACKWARD=mma for N >= 9)
        (+ ndg_bwd_bounds / ndg_work_items before, ndg_acc_dequant after: the deterministic
         fixed-point reduction of SPEC.md:294, and the band order of the work items)
     K8 ndg_epilogue      backward tail, raw-parameter chain rule
@@ -345,8 +345,9 @@ class HotPath:
     # The warp-MMA K7 forms z~ with the K5 z-GEMM (same records, same error ~2e-7 * RMS(B)), so it
     # shares the tensor-core forward's bound. Its cost does not depend on N (dims pad to one m16
     # block); the FP32 K7's grows with N and spills from 13 on. Measured (FP32 vs MMA, 50k Gaussians,
-    # 2^18 queries): 122 vs ~208 ms at N=13, 187 vs ~210 at 14, 270 vs 207 at 15, 331 vs 210 at 16.
-    MMA_MIN_N = 15
+    # 2^18 queries, f16 K7-MMA): 126 vs 174 ms at N=13, 182 vs 178 at 14, 281 vs ~176 at 15, 315 vs 176
+    # at 16 (the round-1 tf32 K7-MMA: ~208 at every N).
+    MMA_MIN_N = 14
 
     def backward_mma_ok(self, recs: EvalRecords) -> bool:
         return (self.backward_impl == "mma" and recs.rec_tc is not None

@@ -138,7 +138,7 @@ def test_fwd_bwd_parity(cuda, N, G, B, children, amp_mode, regime, fwd):
     (16, 400, 2048, False, "C"),
 ])
 def test_mma_backward_parity(cuda, N, G, B, children, regime):
-    """Warp-MMA K7 (ndg_backward_mma, the default at N >= 15; forced here down to N = 9) against the float64 oracle, at the
+    """Warp-MMA K7 (ndg_backward_mma, the default at N >= 14; forced here down to N = 9) against the float64 oracle, at the
     default sigma0 (sharper than the tcgen05-moments cases above: z~ is formed in z-space)."""
     ndg = _ndg()
     om, mix, q, t = _mk(N, G, B, children=children, regime=regime)
