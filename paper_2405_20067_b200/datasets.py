@@ -195,7 +195,7 @@ class ShadingToyTarget:
         self.phase = rng.uniform(0, 2 * np.pi, 3)
         self._params = {}
 
-    def __call__(self, q):
+    def __call__(self, q, out=None):
         import ctypes
 
         import torch
@@ -206,7 +206,8 @@ class ShadingToyTarget:
         if p is None:
             p = torch.tensor(np.concatenate([self.freq, self.phase]), dtype=torch.float32, device=q.device)
             self._params[q.device] = p
-        out = torch.empty(q.shape[0], 3, dtype=torch.float32, device=q.device)
+        if out is None:
+            out = torch.empty(q.shape[0], 3, dtype=torch.float32, device=q.device)
         K.call("ndg_shading_target", self.n_dims, int(q.shape[0]), ctypes.c_void_p(q.data_ptr()),
                ctypes.c_void_p(p.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                ctypes.c_void_p(torch.cuda.current_stream(q.device).cuda_stream))
@@ -228,8 +229,8 @@ class QuerySampler:
     def set_state(self, st: dict):
         self.seed, self.draw = int(st["seed"]), int(st["draw"])
 
-    def queries(self, n_dims: int, batch_size: int, tile_size: int, device, rank: int = 0, world: int = 1):
-        """The next global batch, this rank's strided tiles of it."""
+    def queries(self, n_dims: int, batch_size: int, tile_size: int, device, rank: int = 0, world: int = 1, out=None):
+        """The next global batch, this rank's strided tiles of it (into `out` when given)."""
         import ctypes
 
         import torch
@@ -237,7 +238,12 @@ class QuerySampler:
         from . import kernels as K
         T = batch_size // tile_size
         mine = len(range(rank, T, world))
-        q = torch.empty(mine * tile_size, n_dims, dtype=torch.float32, device=device)
+        if out is None:
+            q = torch.empty(mine * tile_size, n_dims, dtype=torch.float32, device=device)
+        else:
+            if tuple(out.shape) != (mine * tile_size, n_dims) or out.dtype != torch.float32 or not out.is_contiguous():
+                raise ValueError("out must be a contiguous float32 [local batch, n_dims] tensor")
+            q = out
         nb = int(K.load().ndg_sample_workspace(batch_size))
         if self._ws is None or self._ws.numel() * 8 < nb or self._ws.device != q.device:
             self._ws = torch.empty((nb + 7) // 8, dtype=torch.int64, device=device)
@@ -249,7 +255,7 @@ class QuerySampler:
 
 
 def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, sampler, device, rank: int = 0,
-                 world: int = 1):
+                 world: int = 1, out=None):
     """SPEC.md:440-448 on the device: fresh uniform queries, sorted by the first (position) dimension
     into contiguous tiles, exact targets. batch_size must be a multiple of tile_size. `sampler` is a
     QuerySampler (or an int seed for a one-off batch); the sort is generated, not performed
@@ -257,7 +263,8 @@ def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, sampler, 
 
     Data-parallel (world > 1): every rank draws the same GLOBAL batch and keeps its strided tiles (global
     tile i -> rank i mod world, parallel.shard_tiles), evaluating the target only there -- so the union
-    over ranks is exactly the 1-GPU batch and the summed gradients equal the 1-GPU step's."""
+    over ranks is exactly the 1-GPU batch and the summed gradients equal the 1-GPU step's.
+    `out` = (queries, targets) buffers to fill (e.g. a GraphedStep's inputs)."""
     if batch_size % tile_size:
         raise ValueError("batch_size must be a multiple of tile_size (SPEC.md:441)")
     T = batch_size // tile_size
@@ -265,5 +272,12 @@ def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, sampler, 
         raise ValueError(f"{T} tiles cannot give each of {world} ranks one (batch_size / tile_size >= world)")
     if not isinstance(sampler, QuerySampler):
         sampler = QuerySampler(int(sampler))
-    q = sampler.queries(n_dims, batch_size, tile_size, device, rank, world)
-    return q, target(q).contiguous()
+    if out is None:
+        q = sampler.queries(n_dims, batch_size, tile_size, device, rank, world)
+        return q, target(q).contiguous()
+    q = sampler.queries(n_dims, batch_size, tile_size, device, rank, world, out=out[0])
+    if isinstance(target, ShadingToyTarget):
+        target(q, out=out[1])
+    else:
+        out[1].copy_(target(q))
+    return out

@@ -676,18 +676,23 @@ class GraphedStep:
         T = int(queries.shape[0]) // hp.tile
         hp._static = dict(cond=self.cond)
         try:
+            # capture_begin / capture_end on a side stream (not the torch.cuda.graph context, which empties
+            # the allocator cache on every capture: a fit re-captures after each refinement event)
+            self.graph = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream(hp.device)
             side.wait_stream(torch.cuda.current_stream(hp.device))
-            with torch.cuda.stream(side):                  # static-mode warm-up off the default stream
-                hp._launch_step(mix, queries, targets, True, n_total, self.grads, None)
-            torch.cuda.current_stream(hp.device).wait_stream(side)
-            self.graph = torch.cuda.CUDAGraph()
-            l0 = K.launch_count
             timed = {k: len(v) for k, v in hp.events.items()} if hp.events is not None else None
-            with torch.cuda.graph(self.graph):
-                recs, cl, pred, qrec, loss, _ = hp._launch_step(mix, queries, targets, True, n_total, self.grads, None)
-                self.readback = torch.cat([hp.status, loss.view(torch.int64), recs.tc_cond.view(torch.int64),
-                                           cl.offsets[T:T + 1], cl.chunk_offsets[T:T + 1]])
+            l0 = K.launch_count
+            with torch.cuda.stream(side):
+                self.graph.capture_begin()
+                try:
+                    recs, cl, pred, qrec, loss, _ = hp._launch_step(mix, queries, targets, True, n_total, self.grads,
+                                                                    None)
+                    self.readback = torch.cat([hp.status, loss.view(torch.int64), recs.tc_cond.view(torch.int64),
+                                               cl.offsets[T:T + 1], cl.chunk_offsets[T:T + 1]])
+                finally:
+                    self.graph.capture_end()
+            torch.cuda.current_stream(hp.device).wait_stream(side)
             self.launches = K.launch_count - l0            # libndg kernels per replay
             # CUDA-event pairs captured around K4 / K5 / K7 (when kernel timing was on at capture)
             self.timed = {} if timed is None else {k: hp.events[k].pop() for k in timed if len(hp.events[k]) > timed[k]}

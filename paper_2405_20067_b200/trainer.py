@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import datasets as D
-from .engine import HotPath, adam_step, new_adam_state
+from .engine import GraphedStep, HotPath, adam_step, new_adam_state
 from .errors import TrainingAborted
 from .gmm import BRIGHTNESS, FLAG_CHILD, FLAG_FROZEN, Mixture, n_chol, raw_slices, raw_width, tri
 
@@ -53,6 +53,7 @@ class TrainConfig:
     cull: bool = True
     n_components: int = 256
     amp_mode: int = BRIGHTNESS
+    graph: bool = True          # replay the step as a CUDA graph when the worst-case list is small (GraphedStep)
 
     def threshold(self) -> float:
         return self.materialize_threshold if self.materialize_threshold is not None else \
@@ -146,14 +147,15 @@ class Trainer:
         self.last_allreduce_bytes = 0
         self.phase_stats = None       # [Gev, 3] float64 on the device: the phase's density statistics
         self.last_good = self.mix.clone()
+        self._gs = None               # the captured step of the current working set (GraphedStep)
+        self._gbuf = None             # its static (queries, targets) buffers
+        self._n_frozen = int(((self.mix.flags & FLAG_FROZEN) != 0).sum())   # host mirror (changes at events)
 
     # -- one iteration -----------------------------------------------------------------------
     def iteration(self) -> MetricsRow:
         cfg = self.cfg
         t0 = time.perf_counter()
-        q, tg = D.sample_batch(self.target, self.n, cfg.batch_size, cfg.tile_size, self.sampler, self.device,
-                               self.rank, self.world)
-        res = self.hp.fwd_bwd(self.mix, q, tg, cull=cfg.cull, n_total=cfg.batch_size, allreduce=self.allreduce)
+        res = self._step()
         self.last_allreduce_bytes = res.grads.reduced().numel() * 4 if self.allreduce is not None else 0
         if not math.isfinite(res.loss):
             self.mix = self.last_good.clone()
@@ -174,6 +176,28 @@ class Trainer:
         ms = (time.perf_counter() - t0) * 1e3
         return MetricsRow(self.step_no, res.loss, int(self.live_components()), 1.0 - res.kept_fraction, ms)
 
+    def _step(self):
+        """sample_batch + fwd_bwd (+ the allreduce). Small working sets (worst-case candidate list <= 2^24)
+        replay one CUDA graph per step (engine.GraphedStep, byte-identical to the eager step), captured
+        again whenever a refinement event replaced the working set; the batch is drawn straight into its
+        input buffers."""
+        cfg = self.cfg
+        T = cfg.batch_size // cfg.tile_size
+        B_local = len(range(self.rank, T, self.world)) * cfg.tile_size
+        if not (cfg.graph and cfg.cull and GraphedStep.eligible(self.hp, self.mix, B_local)):
+            q, tg = D.sample_batch(self.target, self.n, cfg.batch_size, cfg.tile_size, self.sampler, self.device,
+                                   self.rank, self.world)
+            return self.hp.fwd_bwd(self.mix, q, tg, cull=cfg.cull, n_total=cfg.batch_size, allreduce=self.allreduce)
+        if self._gbuf is None:
+            self._gbuf = (torch.empty(B_local, self.n, dtype=torch.float32, device=self.device),
+                          torch.empty(B_local, 3, dtype=torch.float32, device=self.device))
+        qs, ts = self._gbuf
+        D.sample_batch(self.target, self.n, cfg.batch_size, cfg.tile_size, self.sampler, self.device, self.rank,
+                       self.world, out=(qs, ts))
+        if self._gs is None or not self._gs.matches(self.mix):
+            self._gs = GraphedStep(self.hp, self.mix, qs, ts, n_total=cfg.batch_size)
+        return self._gs(allreduce=self.allreduce)
+
     # -- resume state (SPEC.md:505-508, 552: resume is bit-identical) ----------------------------
     def rng_state(self) -> dict:
         """Everything random that the future of the fit depends on: the batch stream's (seed, draw)
@@ -187,7 +211,7 @@ class Trainer:
             self.rng.bit_generator.state = st["numpy"]
 
     def live_components(self) -> int:
-        return int(self.mix.G - int(((self.mix.flags & FLAG_FROZEN) != 0).sum()))   # frozen rows are archived
+        return self.mix.G - self._n_frozen         # frozen rows are archived at events (host mirror, no sync)
 
     # -- refinement events ---------------------------------------------
     def density_summary(self) -> dict:
@@ -224,6 +248,7 @@ class Trainer:
         """Move frozen rows (out of optimisation and evaluation) to the archive."""
         fr = (self.mix.flags & FLAG_FROZEN) != 0
         if not bool(fr.any()):
+            self._n_frozen = 0
             return 0
         keep = ~fr
         moved = dict(params=self.mix.params[fr], child=self.mix.child[fr], flags=self.mix.flags[fr], ids=self.ids[fr])
@@ -235,6 +260,7 @@ class Trainer:
         self.state = {k: v[keep].contiguous() for k, v in self.state.items()}
         self.low_count = self.low_count[keep].contiguous()
         self.ids = self.ids[keep].contiguous()
+        self._n_frozen = 0
         return int(fr.sum())
 
     def _merged(self, active: dict, archived: dict):
