@@ -46,6 +46,15 @@ def _target(cfg: dict, n_dims: int, device):
     if kind == "gmm":
         return D.GmmOracleTarget(int(data.get("target_seed", 0)), n_dims, int(data.get("target_components", 8)),
                                  device=device)
+    if kind == "file":                       # an NDGT tensor file
+        if "path" not in data:
+            raise ConfigError("data.target = file needs data.path", field="path")
+        ds = D.FileDataset.from_ndgt(str(data["path"]), seed=int(data.get("target_seed", 0)),
+                                     perturb_sigma=float(data.get("perturb_sigma", 0.0)), device=device)
+        if ds.n_dims != n_dims:
+            raise ConfigError(f"data.n_dims = {n_dims} but {data['path']} holds {ds.n_dims}-D queries",
+                              field="n_dims")
+        return ds
     raise ConfigError(f"unknown target {kind!r}", field="target")
 
 

@@ -254,6 +254,106 @@ class QuerySampler:
         return q
 
 
+class FileDataset:
+    """A tensor-file source: fixed queries [M, N] and targets [M, 3] resident in
+    HBM. sample_batch draws random slices without replacement within an epoch (a fresh device-side
+    permutation per epoch, seeded by (seed, epoch); a batch that runs past the end takes the rest and
+    continues in the reshuffled next epoch), sorts the slice by the first (position) dimension into
+    tiles, and -- when perturb_sigma > 0 -- adds clamped Gaussian noise of that scale to the
+    direction-tagged dimensions of the queries only (perturb_directions). Its whole
+    state is (seed, epoch, position, draw): four integers in the checkpoint."""
+
+    def __init__(self, queries, targets, roles=None, *, seed: int = 0, perturb_sigma: float = 0.0, device=None):
+        import torch
+        q = torch.as_tensor(np.ascontiguousarray(queries, np.float32))
+        t = torch.as_tensor(np.ascontiguousarray(targets, np.float32))
+        if q.ndim != 2 or t.shape != (q.shape[0], 3):
+            raise ValueError("queries [M, N] and targets [M, 3] required")
+        if perturb_sigma < 0:
+            raise ValueError("perturb_sigma must be >= 0")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.q, self.t = q.to(self.device), t.to(self.device)
+        self.n_dims, self.count = int(q.shape[1]), int(q.shape[0])
+        self.roles = list(roles) if roles is not None else [3] * self.n_dims
+        self.dir_dims = [i for i, r in enumerate(self.roles) if r == 1]          # formats.ROLES["direction"]
+        self.seed, self.perturb_sigma = int(seed), float(perturb_sigma)
+        self.epoch, self.pos, self.draw = 0, 0, 0
+        self._perm = None
+
+    @classmethod
+    def from_ndgt(cls, path, **kw):
+        from .formats import read_ndgt
+        q, t, roles = read_ndgt(path)
+        return cls(q, t, roles, **kw)
+
+    def state(self) -> dict:
+        return dict(seed=self.seed, epoch=self.epoch, pos=self.pos, draw=self.draw)
+
+    def set_state(self, st: dict):
+        self.seed, self.epoch, self.pos, self.draw = (int(st["seed"]), int(st["epoch"]), int(st["pos"]),
+                                                      int(st["draw"]))
+        self._perm = None
+
+    _TAGS = {"epoch": 1, "perturb": 2, "init": 3}
+
+    def _generator(self, tag: str, value: int = 0):
+        """A device generator seeded by splitmix64 of (seed, tag, value): deterministic across processes."""
+        import torch
+        x = 0
+        for v in (self.seed, self._TAGS[tag], value):
+            x = (x ^ (v & 0xFFFFFFFFFFFFFFFF)) + 0x9E3779B97F4A7C15 & 0xFFFFFFFFFFFFFFFF
+            x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9 & 0xFFFFFFFFFFFFFFFF
+            x = (x ^ (x >> 27)) * 0x94D049BB133111EB & 0xFFFFFFFFFFFFFFFF
+            x ^= x >> 31
+        g = torch.Generator(device=self.device)
+        g.manual_seed(x & ((1 << 63) - 1))
+        return g
+
+    def _permutation(self):
+        import torch
+        if self._perm is None or self._perm[0] != self.epoch:
+            self._perm = (self.epoch, torch.randperm(self.count, generator=self._generator("epoch", self.epoch),
+                                                     device=self.device))
+        return self._perm[1]
+
+    def _next_indices(self, B: int):
+        import torch
+        parts, need = [], B
+        while need:
+            take = min(need, self.count - self.pos)
+            parts.append(self._permutation()[self.pos:self.pos + take])
+            self.pos += take
+            need -= take
+            if self.pos == self.count:                     # epoch wrap: reshuffle
+                self.epoch, self.pos = self.epoch + 1, 0
+        return parts[0] if len(parts) == 1 else torch.cat(parts)
+
+    def points(self, count: int):
+        """`count` dataset points (initial means): the first of a seeded permutation."""
+        import torch
+        perm = torch.randperm(self.count, generator=self._generator("init"), device=self.device)
+        return self.q[perm[:min(count, self.count)]]
+
+    def batch(self, batch_size: int, tile_size: int, rank: int = 0, world: int = 1, out=None):
+        import torch
+        idx = self._next_indices(batch_size)
+        q = self.q[idx]
+        if self.perturb_sigma > 0 and self.dir_dims:
+            d = torch.tensor(self.dir_dims, device=self.device)
+            noise = torch.randn(batch_size, len(self.dir_dims), generator=self._generator("perturb", self.draw),
+                                device=self.device) * self.perturb_sigma
+            q[:, d] = (q[:, d] + noise).clamp_(0.0, 1.0)
+        self.draw += 1
+        order = torch.sort(q[:, 0], stable=True).indices      # tiles from spatially sorted queries
+        T = batch_size // tile_size
+        order = order.view(T, tile_size)[rank::world].reshape(-1)
+        if out is None:
+            return q[order].contiguous(), self.t[idx[order]].contiguous()
+        torch.index_select(q, 0, order, out=out[0])
+        torch.index_select(self.t, 0, idx[order], out=out[1])
+        return out
+
+
 def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, sampler, device, rank: int = 0,
                  world: int = 1, out=None):
     """SPEC.md:440-448 on the device: fresh uniform queries, sorted by the first (position) dimension
@@ -270,6 +370,8 @@ def sample_batch(target, n_dims: int, batch_size: int, tile_size: int, sampler, 
     T = batch_size // tile_size
     if world > 1 and T < world:
         raise ValueError(f"{T} tiles cannot give each of {world} ranks one (batch_size / tile_size >= world)")
+    if isinstance(target, FileDataset):                     # file source: its own epoch / slice state
+        return target.batch(batch_size, tile_size, rank, world, out=out)
     if not isinstance(sampler, QuerySampler):
         sampler = QuerySampler(int(sampler))
     if out is None:

@@ -22,7 +22,7 @@ SECTIONS = {
                 "lr_color", "lr_amp", "beta1", "beta2", "adam_eps", "batch_size", "seed", "n_components",
                 "amp_mode", "loss_eps"),
     "culling": ("k", "multiplier", "tile_size", "cull"),
-    "data": ("target", "n_dims", "target_components", "target_seed"),
+    "data": ("target", "n_dims", "target_components", "target_seed", "path", "perturb_sigma"),
     # cmd_bench_cull: synthetic workload + the sweep (comma-separated lists)
     "bench": ("gaussians", "queries", "regime", "sigma0", "seed", "k_list", "multiplier_list", "tile_list", "reps",
               "epsilon"),
@@ -42,7 +42,7 @@ def _convert(raw: str, line: int, field: str):
             return cast(v)
         except ValueError:
             pass
-    if v and all(c.isalnum() or c in "_-." for c in v):
+    if v and all(c.isalnum() or c in "_-./" for c in v):
         return v
     raise ConfigError(f"line {line}: cannot parse value {raw!r} for {field}", line=line, field=field)
 

@@ -129,7 +129,9 @@ class Trainer:
         self.sampler = D.QuerySampler(cfg.seed * 1000003 + 1)
         self.rng = np.random.default_rng(cfg.seed)
         self.allreduce, self.rank, self.world = allreduce, rank, world
-        if mixture is None:
+        if mixture is None and isinstance(target, D.FileDataset):
+            mixture = initial_mixture(cfg, n_dims, target.points(cfg.n_components), self.device)
+        elif mixture is None:
             # initial means from data points: a one-off draw, identical on every rank; the
             # first coordinate of a sorted draw is ordered, so pick the points by a seeded permutation
             q0 = D.QuerySampler(cfg.seed).queries(n_dims, max(cfg.tile_size, cfg.n_components), 1, self.device)
@@ -201,12 +203,18 @@ class Trainer:
     # -- resume state (resume is bit-identical) ----------------------------
     def rng_state(self) -> dict:
         """Everything random that the future of the fit depends on: the batch stream's (seed, draw)
-        (identical on every rank) and the full numpy PCG64 state of the spawn RNG."""
-        return dict(seed=self.cfg.seed, sampler=self.sampler.state(), numpy=self.rng.bit_generator.state)
+        (identical on every rank; for a file source its (seed, epoch, position, draw)) and the full numpy
+        PCG64 state of the spawn RNG."""
+        st = dict(seed=self.cfg.seed, sampler=self.sampler.state(), numpy=self.rng.bit_generator.state)
+        if isinstance(self.target, D.FileDataset):
+            st["dataset"] = self.target.state()
+        return st
 
     def set_rng_state(self, st: dict):
         if isinstance(st.get("sampler"), dict):
             self.sampler.set_state(st["sampler"])
+        if isinstance(st.get("dataset"), dict) and isinstance(self.target, D.FileDataset):
+            self.target.set_state(st["dataset"])
         if isinstance(st.get("numpy"), dict):
             self.rng.bit_generator.state = st["numpy"]
 

@@ -77,3 +77,9 @@ def test_checkpoint_byte_identical(tmp_path):
     with pytest.raises(FileFormatError):
         (tmp_path / "t.ndgc").write_bytes(a.read_bytes()[:-3])
         F.load_checkpoint(tmp_path / "t.ndgc")
+
+
+def test_config_file_dataset_keys():
+    """data.target = file with a path (slashes allowed in bare values) and the direction perturbation."""
+    cfg = F.parse_config("[data]\ntarget = file\npath = /data/run-1/train_q.ndgt\nn_dims = 6\nperturb_sigma = 0.02\n")
+    assert cfg["data"] == dict(target="file", path="/data/run-1/train_q.ndgt", n_dims=6, perturb_sigma=0.02)
