@@ -69,3 +69,23 @@ def test_shading_target_matches_oracle(cuda, n):
     ref = O.shading_toy(q.cpu().numpy(), tgt.freq, tgt.phase)
     assert got.shape == (1 << 15, 3) and got.dtype == np.float32
     assert np.max(np.abs(got - ref)) < 2e-5, np.max(np.abs(got - ref))
+
+
+def test_sorted_tiling_culls_at_least_random_tiling(cuda):
+    """on a 10k-component mixture, tiles of queries sorted by the first position dimension
+    cull a larger or equal fraction than random tiles of the same queries, on average over 100 batches."""
+    import paper_2405_20067_b200 as ndg
+    D = _D()
+    om, _ = O.synthetic_mixture(6, 10000, seed=1, sigma0=0.05)
+    mix = ndg.Mixture.from_arrays(6, om.amp_mode, om.params)
+    hp = ndg.HotPath(6, projection_seed=2)
+    recs = hp.activate(mix)
+    pb = hp.project(recs)
+    s = D.QuerySampler(21)
+    kept_sorted, kept_random = [], []
+    for b in range(100):
+        q = s.queries(6, 4096, 256, "cuda")
+        perm = torch.randperm(4096, generator=torch.Generator(device="cuda").manual_seed(b), device="cuda")
+        for qq, acc in ((q, kept_sorted), (q[perm].contiguous(), kept_random)):
+            acc.append(hp.cull(hp.tile_bounds(qq), pb).kept_fraction(recs.Gev))
+    assert np.mean(kept_sorted) <= np.mean(kept_random), (np.mean(kept_sorted), np.mean(kept_random))
