@@ -65,6 +65,15 @@ __host__ __device__ constexpr int acc_flag(int n) { return n_chol(n) + n; }
 __host__ __device__ constexpr int acc_tail(int n) { return n_chol(n) + n + 1; }
 __host__ __device__ constexpr int acc_doubles(int n) { return acc_tail(n) + 3 + kNumStats; }
 
+// Threads per CTA for a thread-per-item kernel: the largest power of two <= max_threads that still gives
+// every SM two CTAs, at least 32 -- small configurations (cfg1: 4096 Gaussians) then spread over ~128
+// SMs instead of running 128-thread CTAs on 32 of them.
+__host__ __device__ constexpr int spread_threads(int64_t items, int max_threads) {
+    int t = max_threads;
+    while (t > 32 && (items + t - 1) / t < 2 * 148) t >>= 1;
+    return t;
+}
+
 // Backward work items in band order (ndg_work_items): bands of kBand tiles run chunk-major.
 constexpr int kBand = 512;
 

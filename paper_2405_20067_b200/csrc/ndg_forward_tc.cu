@@ -483,40 +483,55 @@ __global__ void tc_records_kernel(int n, int64_t Gev, const double* __restrict__
                                   const float* __restrict__ rec, float* __restrict__ rec_tc,
                                   double* __restrict__ cond) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= Gev) return;
-    const int P = n_chol(n), K = tc_k(n), RT = tc_rec_floats(n);
-    float* out = rec_tc + e * RT;
-    for (int t = 0; t < RT; ++t) out[t] = 0.f;
-    if (!(eflags[e] & 1)) return;
-    for (int ch = 0; ch < 3; ++ch) out[n * K + ch] = rec[e * rec_floats(n) + rec_a(n) + ch];   // colour a
-    double L[n_chol(NMAX)], W[n_chol(NMAX)];
-    for (int t = 0; t < P; ++t) L[t] = chol64[e * P + t];
-    for (int j = 0; j < n; ++j)                     // W = L^-1 (lower), column by column
-        for (int i = j; i < n; ++i) {
-            double acc = (i == j) ? 1.0 : 0.0;
-            for (int k = j; k < i; ++k) acc -= L[tri(i, k)] * W[tri(k, j)];
-            W[tri(i, j)] = acc / L[tri(i, i)];
+    double b = -1.0;                                  // this Gaussian's B_e (< 0: not counted)
+    if (e < Gev) {
+        const int P = n_chol(n), K = tc_k(n), RT = tc_rec_floats(n);
+        float* out = rec_tc + e * RT;
+        for (int t = 0; t < RT; ++t) out[t] = 0.f;
+        if (eflags[e] & 1) {
+            for (int ch = 0; ch < 3; ++ch) out[n * K + ch] = rec[e * rec_floats(n) + rec_a(n) + ch];   // colour a
+            double L[n_chol(NMAX)], W[n_chol(NMAX)];
+            for (int t = 0; t < P; ++t) L[t] = chol64[e * P + t];
+            for (int j = 0; j < n; ++j)                     // W = L^-1 (lower), column by column
+                for (int i = j; i < n; ++i) {
+                    double acc = (i == j) ? 1.0 : 0.0;
+                    for (int k = j; k < i; ++k) acc -= L[tri(i, k)] * W[tri(k, j)];
+                    W[tri(i, j)] = acc / L[tri(i, i)];
+                }
+            // plane-major: element (row i, column k) at ((k / 4) * n + i) * 4 + k % 4
+            auto at = [&](int i, int k) -> float& { return out[((k / 4) * n + i) * 4 + (k & 3)]; };
+            double bound = 0.0;
+            for (int i = 0; i < n; ++i) {
+                double bias = 0.0, lin = 0.0;
+                for (int j = 0; j <= i; ++j) {
+                    const double w = kC * W[tri(i, j)];
+                    at(i, j) = (float)w;
+                    bias += w * (0.5 - mean64[e * n + j]);
+                    lin += fabs(w);
+                }
+                at(i, n) = (float)bias;
+                bound = fmax(bound, 0.5 * lin + fabs(bias));
+            }
+            if (!(eflags[e] & 2)) b = isfinite(bound) ? bound : 1.0e300;
         }
-    // plane-major: element (row i, column k) at ((k / 4) * n + i) * 4 + k % 4
-    auto at = [&](int i, int k) -> float& { return out[((k / 4) * n + i) * 4 + (k & 3)]; };
-    double bound = 0.0;
-    for (int i = 0; i < n; ++i) {
-        double bias = 0.0, lin = 0.0;
-        for (int j = 0; j <= i; ++j) {
-            const double w = kC * W[tri(i, j)];
-            at(i, j) = (float)w;
-            bias += w * (0.5 - mean64[e * n + j]);
-            lin += fabs(w);
-        }
-        at(i, n) = (float)bias;
-        bound = fmax(bound, 0.5 * lin + fabs(bias));
     }
-    if (cond && !(eflags[e] & 2)) {
-        const double b = isfinite(bound) ? bound : 1.0e300;
-        // positive doubles order like their bit patterns
-        atomicMax(reinterpret_cast<unsigned long long*>(cond), (unsigned long long)__double_as_longlong(b));
-        atomicAdd(cond + 1, b * b);
-        atomicAdd(cond + 2, 1.0);
+    if (cond) {
+        // warp-reduce [max, sum of squares, count] first: one set of atomics per warp, not per Gaussian
+        // (same-address atomics serialise in L2; positive doubles order like their bit patterns)
+        unsigned long long mx = b >= 0.0 ? (unsigned long long)__double_as_longlong(b) : 0ull;
+        double ss = b >= 0.0 ? b * b : 0.0, cnt = b >= 0.0 ? 1.0 : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = m2 > mx ? m2 : mx;
+            ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+        if ((threadIdx.x & 31) == 0 && cnt > 0.0) {
+            atomicMax(reinterpret_cast<unsigned long long*>(cond), mx);
+            atomicAdd(cond + 1, ss);
+            atomicAdd(cond + 2, cnt);
+        }
     }
 }
 
@@ -532,7 +547,8 @@ extern "C" int ndg_tc_records(int n, int64_t Gev, const double* mean64, const do
                               const float* rec, float* rec_tc, double* cond, void* stream) {
     if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
     if (Gev == 0) return NDG_OK;
-    tc_records_kernel<<<(unsigned)((Gev + 127) / 128), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+    const int threads = spread_threads(Gev, 128);
+    tc_records_kernel<<<(unsigned)((Gev + threads - 1) / threads), threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
         n, Gev, mean64, chol64, eflags, rec, rec_tc, cond);
     NDG_CHECK_LAUNCH();
     return NDG_OK;

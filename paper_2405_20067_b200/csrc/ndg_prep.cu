@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <algorithm>
+
 #include "ndg_common.cuh"
 
 using namespace ndg;
@@ -139,7 +141,7 @@ extern "C" int ndg_prologue(int n, int64_t G, int64_t Gev, int amp_mode, const f
     NDG_REQUIRE(G >= 0 && (Gev == G || Gev == 2 * G), "Gev must be G or 2G");
     NDG_REQUIRE(Gev == G || child != nullptr, "child rows required when Gev == 2G");
     if (Gev == 0) return NDG_OK;
-    int threads = 128;
+    const int threads = spread_threads(Gev, 128);
     prologue_kernel<<<(unsigned)((Gev + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
         n, G, Gev, amp_mode, params, child, flags, rec, mean64, chol64, eflags, status);
     NDG_CHECK_LAUNCH();
@@ -152,7 +154,7 @@ extern "C" int ndg_prologue(int n, int64_t G, int64_t Gev, int amp_mode, const f
 __global__ void project_kernel(int n, int64_t Gev, const double* __restrict__ mean64,
                                const double* __restrict__ chol64, const uint8_t* __restrict__ eflags,
                                const double* __restrict__ dirs, int k, double mult, double* __restrict__ m_r,
-                               double* __restrict__ s_r, double* __restrict__ thr) {
+                               double* __restrict__ s_r, double* __restrict__ thr, int kpb) {
     extern __shared__ double sdir[];
     for (int t = threadIdx.x; t < k * n; t += blockDim.x) sdir[t] = dirs[t];
     __syncthreads();
@@ -164,7 +166,8 @@ __global__ void project_kernel(int n, int64_t Gev, const double* __restrict__ me
     for (int t = 0; t < P; ++t) L[t] = chol64[e * P + t];
     const uint8_t f = eflags[e];
     const bool live = f & 1, degenerate = f & 2;
-    for (int ri = 0; ri < k; ++ri) {
+    const int r0 = blockIdx.y * kpb, r1 = min(k, r0 + kpb);   // this CTA's projections (blockIdx.y)
+    for (int ri = r0; ri < r1; ++ri) {
         const double* r = sdir + ri * n;
         double acc = __dmul_rn(m[0], r[0]);
         for (int j = 1; j < n; ++j) acc = __dadd_rn(acc, __dmul_rn(m[j], r[j]));
@@ -187,9 +190,12 @@ extern "C" int ndg_project(int n, int64_t Gev, const double* mean64, const doubl
     if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
     NDG_REQUIRE(k >= 1 && k <= 256, "k must be in 1..256");
     if (Gev == 0) return NDG_OK;
-    int threads = 128;
-    project_kernel<<<(unsigned)((Gev + threads - 1) / threads), threads, sizeof(double) * k * n,
-                     as_stream(stream)>>>(n, Gev, mean64, chol64, eflags, dirs, k, multiplier, m_r, s_r, thr);
+    const int threads = spread_threads(Gev, 128);
+    const int64_t gx = (Gev + threads - 1) / threads;
+    // projections per CTA: all k, or fewer (blockIdx.y) when the Gaussians alone leave SMs idle
+    const int kpb = (int)std::max<int64_t>(1, std::min<int64_t>(k, gx * k / (2 * 148)));
+    project_kernel<<<dim3((unsigned)gx, (unsigned)((k + kpb - 1) / kpb)), threads, sizeof(double) * k * n,
+                     as_stream(stream)>>>(n, Gev, mean64, chol64, eflags, dirs, k, multiplier, m_r, s_r, thr, kpb);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }
@@ -198,7 +204,7 @@ extern "C" int ndg_project(int n, int64_t Gev, const double* mean64, const doubl
 // K3 tile bounds: TileBounds. One CTA per tile, one thread per query.
 // ---------------------------------------------------------------------------------------------
 __global__ void tile_bounds_kernel(int n, int tile, const float* __restrict__ q, const double* __restrict__ dirs,
-                                   int k, double* __restrict__ lo, double* __restrict__ hi) {
+                                   int k, double* __restrict__ lo, double* __restrict__ hi, int kpb) {
     __shared__ double s_lo[32], s_hi[32];
     const int64_t t = blockIdx.x;
     const int qi = threadIdx.x;
@@ -207,7 +213,8 @@ __global__ void tile_bounds_kernel(int n, int tile, const float* __restrict__ q,
 #pragma unroll
     for (int j = 0; j < NMAX; ++j) x[j] = (valid && j < n) ? q[(t * tile + qi) * n + j] : 0.f;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    for (int ri = 0; ri < k; ++ri) {
+    const int r0 = blockIdx.y * kpb, r1 = min(k, r0 + kpb);   // this CTA's projections (blockIdx.y)
+    for (int ri = r0; ri < r1; ++ri) {
         const double* r = dirs + ri * n;
         double acc = __dmul_rn((double)x[0], r[0]);
 #pragma unroll
@@ -244,7 +251,9 @@ extern "C" int ndg_tile_bounds(int n, int64_t B, int tile, const float* queries,
     int64_t T = B / tile;
     if (T == 0) return NDG_OK;
     int threads = ((tile + 31) / 32) * 32;
-    tile_bounds_kernel<<<(unsigned)T, threads, 0, as_stream(stream)>>>(n, tile, queries, dirs, k, lo, hi);
+    const int kpb = (int)std::max<int64_t>(1, std::min<int64_t>(k, T * k / (2 * 148)));   // split k when T is small
+    tile_bounds_kernel<<<dim3((unsigned)T, (unsigned)((k + kpb - 1) / kpb)), threads, 0, as_stream(stream)>>>(
+        n, tile, queries, dirs, k, lo, hi, kpb);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }
@@ -300,8 +309,9 @@ __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int 
                                                                   const double* __restrict__ thr,
                                                                   uint32_t* __restrict__ mask,
                                                                   int64_t* __restrict__ counts,
-                                                                  const unsigned long long* __restrict__ skip) {
-    constexpr int TILES = REG ? kCullTilesReg : kCullTilesSmem;
+                                                                  const unsigned long long* __restrict__ skip,
+                                                                  int tpc) {
+    constexpr int TILES = REG ? kCullTilesReg : kCullTilesSmem;   // tpc <= TILES tiles per CTA
     if (skip && *skip) return;                     // the bucket pre-filter (ndg_cull_prefilter) took this step
     extern __shared__ double sm[];
     double* s_lo = sm;                             // [TILES][k]
@@ -309,8 +319,8 @@ __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int 
     __shared__ int s_cnt[TILES][kCullThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t e = blockIdx.x * (int64_t)kCullThreads + tid;
-    const int64_t t0 = blockIdx.y * (int64_t)TILES;
-    const int ntile = (int)imin64(TILES, T - t0);
+    const int64_t t0 = blockIdx.y * (int64_t)tpc;
+    const int ntile = (int)imin64(tpc, T - t0);
     for (int x = tid; x < ntile * k; x += kCullThreads) {
         s_lo[x] = lo[t0 * k + x];
         s_hi[x] = hi[t0 * k + x];
@@ -379,7 +389,11 @@ int cull_mask_launch(int64_t T, int k, int64_t Gev, const double* lo, const doub
     if (T == 0 || Gev == 0) return NDG_OK;
     const bool reg = k <= kCullRegK;
     const int tiles = reg ? kCullTilesReg : kCullTilesSmem;
-    dim3 grid((unsigned)((Gev + kCullThreads - 1) / kCullThreads), (unsigned)((T + tiles - 1) / tiles));
+    // tiles per CTA: up to `tiles` (amortises the per-Gaussian bound loads), fewer when that would leave
+    // SMs idle (small configurations: cfg1's 16 Gaussian blocks x 64 tiles would run on 16 SMs)
+    const int64_t gx = (Gev + kCullThreads - 1) / kCullThreads;
+    const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, T * gx / (2 * 148)));
+    dim3 grid((unsigned)gx, (unsigned)((T + tpc - 1) / tpc));
     NDG_REQUIRE(grid.y <= 65535, "too many tiles for one cull launch");
     const size_t smem = sizeof(double) * 2 * tiles * k;    // <= 64 KB at k = 256
     static DeviceOnce attr_set;
@@ -388,9 +402,11 @@ int cull_mask_launch(int64_t T, int k, int64_t Gev, const double* lo, const doub
         cudaFuncSetAttribute(cull_mask_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     }
     if (reg)
-        cull_mask_kernel<true><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts, skip);
+        cull_mask_kernel<true><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts, skip,
+                                                                     tpc);
     else
-        cull_mask_kernel<false><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts, skip);
+        cull_mask_kernel<false><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts, skip,
+                                                                      tpc);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }
@@ -838,7 +854,7 @@ extern "C" int ndg_epilogue(int n, int64_t G, int64_t Gev, int amp_mode, const f
     NDG_REQUIRE(Gev == G || Gev == 2 * G, "Gev must be G or 2G");
     NDG_REQUIRE(Gev == G || (child && grad_child), "child rows and child gradients required when Gev == 2G");
     if (G == 0) return NDG_OK;
-    int threads = 64;
+    const int threads = spread_threads(G, 64);
     epilogue_kernel<<<(unsigned)((G + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
         n, G, Gev, amp_mode, params, child, flags, eflags, chol64, accum, grad_params,
         Gev == 2 * G ? grad_child : nullptr, stats, status);
