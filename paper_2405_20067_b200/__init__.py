@@ -18,7 +18,7 @@ finite_diff_grad, adam_step.
 from .errors import (ConfigError, DegenerateSliceError, FileFormatError, InvalidParameterError,  # noqa: F401
                      NdgError, NonFiniteGradientError, TrainingAborted)
 from .gmm import BRIGHTNESS, OPACITY, Mixture, n_chol, raw_slices, raw_width, tri  # noqa: F401
-from .engine import (CandidateLists, EvalRecords, GradientBuffer, GraphedStep, HotPath, ProjectedBounds,  # noqa: F401
+from .engine import (CandidateLists, EvalRecords, GradientBuffer, GraphedEval, GraphedStep, HotPath, ProjectedBounds,  # noqa: F401
                      ProjectionSet, StepResult, TileBounds, adam_step, alloc_gradients, kept_pairs_flops,
                      make_projection_set, new_adam_state)
 

@@ -734,6 +734,42 @@ class GraphedStep:
                                float(host[4:5].view(torch.float64)[0]), allreduce is not None, check)
 
 
+class GraphedEval:
+    """HotPath.evaluate captured as a CUDA graph for a FIXED mixture and query buffer -- a procedural
+    target (datasets.GmmOracleTarget) evaluated at every training step's batch. Nothing is read back: the
+    mixture does not change, so its status and its conditioning-dependent kernel choice are checked once,
+    by the eager evaluation at capture. Each call writes the mixture's values at `queries` into `out`."""
+
+    def __init__(self, hp: HotPath, mix: Mixture, queries, out, *, cull: bool = False):
+        B = int(queries.shape[0])
+        if B % hp.tile or tuple(out.shape) != (B, 3):
+            raise ValueError("queries must be a tile multiple and out [B, 3]")
+        hp.evaluate(mix, queries, cull=cull)           # eager: status check + the kernel choice
+        cond = hp._recs.tc_cond_host
+        hp._static = dict(cond=cond)
+        try:
+            self.graph = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(hp.device)
+            side.wait_stream(torch.cuda.current_stream(hp.device))
+            with torch.cuda.stream(side):
+                self.graph.capture_begin()
+                try:
+                    hp.reset_status()
+                    recs = hp.activate(mix)
+                    T = B // hp.tile
+                    cl = hp.cull(hp.tile_bounds(queries), hp.project(recs)) if cull else hp.all_active(T, recs)
+                    pred, _, _ = hp.forward(queries, recs, cl)
+                    out.copy_(pred)
+                finally:
+                    self.graph.capture_end()
+            torch.cuda.current_stream(hp.device).wait_stream(side)
+        finally:
+            hp._static = None
+
+    def __call__(self):
+        self.graph.replay()
+
+
 def adam_step(mix: Mixture, grads: GradientBuffer, state, step: int, lr=(2e-3, 5e-3, 1e-2, 1e-2),
               betas=(0.9, 0.999), eps=1e-8):
     """K9: bias-corrected Adam with per-block learning rates, applied to

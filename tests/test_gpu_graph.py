@@ -85,3 +85,17 @@ def test_graph_reports_invalid_parameters(cuda):
     with pytest.raises(ndg.InvalidParameterError) as ei:
         gs()
     assert ei.value.component == 17
+
+
+def test_graphed_eval_equals_eager_target(cuda):
+    """GmmOracleTarget.evaluate_into replays a captured evaluation (no read-back) into the caller's buffer:
+    byte-identical to the eager evaluation, for new queries drawn into the same buffer."""
+    from paper_2405_20067_b200 import datasets as D
+    tgt = D.GmmOracleTarget(3, 6, 8)
+    q = torch.empty(2048, 6, device="cuda")
+    out = torch.empty(2048, 3, device="cuda")
+    s = D.QuerySampler(4)
+    for _ in range(3):
+        s.queries(6, 2048, 256, "cuda", out=q)
+        tgt.evaluate_into(q, out)
+        assert torch.equal(out, tgt(q))
