@@ -34,9 +34,12 @@ def _cases(n_cases=int(os.environ.get("NDG_FUZZ_CASES", "24")), seed=int(os.envi
 
 
 def _rel(a, b, floor=1e-30):
-    """Block-relative error; blocks whose reference norm is below `floor` (values under float32's
-    normal range, which the kernels flush to zero -- e.g. one 16-D Gaussian with g ~ e^-87 at every
-    query) are compared absolutely against the floor."""
+    """Block-relative error; blocks whose reference norm is below `floor` are compared absolutely against
+    the floor. The fwd_bwd cases use floor = 1e-12 x the step's gradient scale (sum over the batch of
+    |dL/dpred|_1 + |ell|): a block that small belongs to Gaussians that no query reaches (g ~ e^-60 at
+    every pair, e.g. a single 15-D Gaussian 9 sigma from all queries), whose numerically-zero gradients
+    float32 resolves only to the z-GEMM's conditioning (error ~ |z~| B_e 2e-7 per pair) -- twelve orders
+    below anything Adam (eps 1e-8) can act on."""
     a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), floor))
 
@@ -59,12 +62,14 @@ def test_fuzz_fwd_bwd(cuda, case):
     assert _rel(res.pred.cpu().numpy(), ref["pred"]) < RTOL
     assert abs(res.loss - ref["loss"]) <= RTOL * max(abs(ref["loss"]), 1e-30)
     ms, cs, cols, amp = O.raw_slices(c["N"])
+    floor = max(1e-30, 1e-12 * float(np.abs(ref["dpred"]).sum() + np.abs(ref["ell"]).sum()))
     for tag, got, want in (("parent", res.grads.params, ref["grad_parent"]), ("child", res.grads.child, ref["grad_child"])):
         if tag == "child" and not c["children"]:
             continue
         g = got.cpu().numpy()
         for name, sl in (("mean", ms), ("chol", cs), ("color", cols), ("amp", slice(amp, amp + 1))):
-            assert _rel(g[:, sl], want[:, sl]) < RTOL, f"{tag}.{name}"
+            assert _rel(g[:, sl], want[:, sl], floor) < RTOL, f"{tag}.{name}"
     st = res.grads.stats.cpu().numpy()
-    for j in range(3):
-        assert _rel(st[:, j], ref["stats"][:, j]) < RTOL, f"stat {j}"
+    for j in range(2):
+        assert _rel(st[:, j], ref["stats"][:, j], floor) < RTOL, f"stat {j}"
+    assert np.array_equal(st[:, 2], ref["stats"][:, 2]), "pair counts"
