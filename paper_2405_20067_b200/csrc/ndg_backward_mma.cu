@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
     for (int gb = warp * kGpw; gb < n_here; gb += 4 * kGpw) {
         // ---- per-Gaussian operands (warp-uniform Gaussian; an absent second one runs on zeros) ----
         uint32_t ah[kGpw][4], al[kGpw][4];   // Ahat 16 x 16 fragment (rows = dims of z~, k = input dims)
-        float bz[kGpw][2], col[kGpw][3], s2[kGpw], rsc[kGpw], zsc[kGpw];
+        float bz[kGpw][2], col[kGpw][3], s2[kGpw], rsc[kGpw];
+        int ses[kGpw];
         int64_t e[kGpw];
         bool live[kGpw];
 #pragma unroll
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
             for (int ch = 0; ch < 3; ++ch) col[j][ch] = live[j] ? __ldg(r + N * K + ch) : 0.f;
             s2[j] = pow2f(-2 * se);                      // |z~|^2 = 2^-2se |z'|^2
             rsc[j] = pow2f(tv - se);                     // v' = 2^tv sqrt|w| z~ = 2^(tv-se) sqrt|w| z'
-            zsc[j] = pow2f(-se);
+            ses[j] = se;
         }
         // the owned Gaussian's per-query constants
         const float o_s2 = oj ? s2[1] : s2[0], o_rsc = oj ? rsc[1] : rsc[0];
@@ -231,7 +232,9 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
             // the owned pair's scalars
             const float gm = ex2_neg(sm);
             const float wm = gm * fmaf(q.z, o_c2, fmaf(q.y, o_c1, q.x * o_c0));
-            const float rm = sqrt_approx(fabsf(wm)) * o_rsc;
+            // sqrt|w| (scaled) carrying the sign of w: one value per query to distribute
+            const float rm = __uint_as_float(__float_as_uint(sqrt_approx(fabsf(wm)) * o_rsc) |
+                                             (__float_as_uint(wm) & 0x80000000u));
             gA[0] = fmaf(gm, q.x, gA[0]);
             gA[1] = fmaf(gm, q.y, gA[1]);
             gA[2] = fmaf(gm, q.z, gA[2]);
@@ -242,15 +245,17 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                 uint32_t ph[2][2], pl[2][2], am[2];      // [n-tile][dims gid | gid+8] packed v' hi / lo
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                    // w, sqrt|w| of queries 2tig (a) and 2tig+1 (b) from their owners (same tig column)
+                    // signed sqrt|w| of queries 2tig (a) and 2tig+1 (b) from their owners (same tig column)
                     const int src = ((j | (u << 1)) << 2) | tig;
-                    const float wa = __shfl_sync(0xffffffffu, wm, src), wb = __shfl_sync(0xffffffffu, wm, src | 16);
                     const float ra = __shfl_sync(0xffffffffu, rm, src), rb = __shfl_sync(0xffffffffu, rm, src | 16);
-                    tz[j][0] = fmaf(wa, z[j][u][0], fmaf(wb, z[j][u][1], tz[j][0]));
-                    tz[j][1] = fmaf(wa, z[j][u][2], fmaf(wb, z[j][u][3], tz[j][1]));
-                    split_h2(ra * z[j][u][0], rb * z[j][u][1], ph[u][0], pl[u][0]);
-                    split_h2(ra * z[j][u][2], rb * z[j][u][3], ph[u][1], pl[u][1]);
-                    am[u] = ((__float_as_uint(wa) & 0x80000000u) >> 16) | (__float_as_uint(wb) & 0x80000000u);
+                    const float v0 = fabsf(ra) * z[j][u][0], v1 = fabsf(rb) * z[j][u][1];
+                    const float v2 = fabsf(ra) * z[j][u][2], v3 = fabsf(rb) * z[j][u][3];
+                    // t' += w z' as (sign sqrt|w|) (sqrt|w| z') = rsc^2 w z', unscaled at the flush
+                    tz[j][0] = fmaf(ra, v0, fmaf(rb, v1, tz[j][0]));
+                    tz[j][1] = fmaf(ra, v2, fmaf(rb, v3, tz[j][1]));
+                    split_h2(v0, v1, ph[u][0], pl[u][0]);
+                    split_h2(v2, v3, ph[u][1], pl[u][1]);
+                    am[u] = ((__float_as_uint(ra) & 0x80000000u) >> 16) | (__float_as_uint(rb) & 0x80000000u);
                 }
                 // MMA2: A = s v'_h (16 dims x 16 queries), B = v'_h | v'_l (16 queries x 8 dims) per column block
                 const uint32_t a2[4] = {ph[0][0] ^ am[0], ph[0][1] ^ am[0], ph[1][0] ^ am[1], ph[1][1] ^ am[1]};
@@ -287,7 +292,8 @@ __global__ void __launch_bounds__(kThreads, NDG_MMA_MINB)
                                (S[j][nb][v] + Mx[j][nb][v] + sMm[colj * 17 + row]) * sS, fx.h);
                 }
             __syncwarp();
-            float r[2] = {tz[j][0] * zsc[j], tz[j][1] * zsc[j]};
+            const float ts = pow2f(min(max(-tv, -126), 127)) * pow2f(min(max(ses[j] - tv, -126), 127));
+            float r[2] = {tz[j][0] * ts, tz[j][1] * ts};     // t' = tz 2^-se / rsc^2 = tz 2^(se - 2 tv)
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 r[i] += __shfl_xor_sync(0xffffffffu, r[i], 1);
