@@ -301,7 +301,7 @@ constexpr int kCullRegK = 16;          // k handled from registers
 constexpr int kCullTilesReg = 64;      // tiles per CTA on the register path (amortises the (m_r, thr) loads)
 constexpr int kCullTilesSmem = 16;
 
-template <bool REG>
+template <bool REG, bool FULL>
 __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int k, int64_t Gev,
                                                                   const double* __restrict__ lo,
                                                                   const double* __restrict__ hi,
@@ -310,8 +310,9 @@ __global__ void __launch_bounds__(kCullThreads) cull_mask_kernel(int64_t T, int 
                                                                   uint32_t* __restrict__ mask,
                                                                   int64_t* __restrict__ counts,
                                                                   const unsigned long long* __restrict__ skip,
-                                                                  int tpc) {
-    constexpr int TILES = REG ? kCullTilesReg : kCullTilesSmem;   // tpc <= TILES tiles per CTA
+                                                                  int tpc_rt) {
+    constexpr int TILES = REG ? kCullTilesReg : kCullTilesSmem;
+    const int tpc = FULL ? TILES : tpc_rt;       // tiles per CTA (FULL: the compile-time maximum)
     if (skip && *skip) return;                     // the bucket pre-filter (ndg_cull_prefilter) took this step
     extern __shared__ double sm[];
     double* s_lo = sm;                             // [TILES][k]
@@ -398,15 +399,25 @@ int cull_mask_launch(int64_t T, int k, int64_t Gev, const double* lo, const doub
     const size_t smem = sizeof(double) * 2 * tiles * k;    // <= 64 KB at k = 256
     static DeviceOnce attr_set;
     if (attr_set.first()) {
-        cudaFuncSetAttribute(cull_mask_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        cudaFuncSetAttribute(cull_mask_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(cull_mask_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(cull_mask_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(cull_mask_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(cull_mask_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     }
-    if (reg)
-        cull_mask_kernel<true><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts, skip,
-                                                                     tpc);
+    // the full-CTA case keeps the tile count a compile-time constant (the runtime bound costs 13%)
+    const bool full = tpc == tiles;
+    if (reg && full)
+        cull_mask_kernel<true, true><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts,
+                                                                           skip, tpc);
+    else if (reg)
+        cull_mask_kernel<true, false><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts,
+                                                                            skip, tpc);
+    else if (full)
+        cull_mask_kernel<false, true><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts,
+                                                                            skip, tpc);
     else
-        cull_mask_kernel<false><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts, skip,
-                                                                      tpc);
+        cull_mask_kernel<false, false><<<grid, kCullThreads, smem, stream>>>(T, k, Gev, lo, hi, m_r, thr, mask, counts,
+                                                                             skip, tpc);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }
