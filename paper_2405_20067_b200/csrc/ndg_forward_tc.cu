@@ -17,6 +17,8 @@
 // planes, one lane issues the MMAs of item (chunk, half) into TMEM buffer `half`, eight epilogue
 // warps (4 lane quarters x 2 Gaussian groups) drain TMEM (2 x 224 accumulator + 64 A columns = 512).
 // The hand-off timeline (tools/tc_trace.py) shows the tensor pipe ~85% busy per chunk.
+#include <algorithm>
+
 #include "ndg_tc.cuh"
 
 using namespace ndg;
@@ -46,6 +48,20 @@ constexpr int kTcStaging = NDG_TC_STAGING;   // raw-record staging ring depth (c
 constexpr int kTBuf = 2;                      // TMEM accumulator buffers: one per query half
 
 constexpr int kARing = 8;                     // colour ring depth (independent of the B ring)
+constexpr int kMaxCluster = 2;                // CTAs per tile when the batch has fewer tiles than SMs
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// float at the same shared-memory offset in cluster CTA `rank` (distributed shared memory)
+__device__ __forceinline__ float ld_cluster_f32(const float* p, int rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+    return v;
+}
 
 #ifdef NDG_TCX_TRACE
 // Timeline probe (tuning builds only): clock64 at each hand-off of the first kTrC chunks of one CTA.
@@ -109,12 +125,13 @@ constexpr size_t tc_smem_bytes() {
 // record into the staging ring), 1 = TMEM allocator + MMA issuer, 2..kEpi0-1 = splitters (staging ->
 // hi/lo K-major B planes + colours), kEpi0..kEpi0+7 = epilogue (warp w: Gaussian group (w-kEpi0)/4,
 // TMEM lane quarter w%4; the A-operand prologue writes query half (w-kEpi0)/4).
-template <int N>
+template <int N, int CS>
 __global__ void __launch_bounds__(kTcThreads, 1)
     forward_tc_kernel(int tile, const float* __restrict__ queries, const float* __restrict__ targets,
                       const float* __restrict__ rec_tc, const int64_t* __restrict__ offsets,
                       const int32_t* __restrict__ idx, float eps, double inv3n, float* __restrict__ pred,
                       float* __restrict__ qrec, double* __restrict__ loss_partial) {
+    constexpr int cs = CS;   // CTAs per tile (a cluster when > 1); 1 compiles to the single-CTA kernel
     using Cfg = TcCfg<N>;
     constexpr int K = Cfg::K, P = Cfg::P, KS = Cfg::KS, C = Cfg::C, RT = Cfg::RT, STG = Cfg::STG;
     constexpr int kNCol = Cfg::NCOL, kA0 = Cfg::A0;
@@ -134,9 +151,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __shared__ float s_pp[256 * 3];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t t = blockIdx.x;
+    // cs > 1 (few tiles): a cluster of cs CTAs per tile, CTA `rank` taking the tile's chunks rank, rank + cs,
+    // ...; every ring below counts the CTA's own chunks (local index c, global chunk gch(c))
+    const int64_t t = CS == 1 ? (int64_t)blockIdx.x : (int64_t)(blockIdx.x / CS);
+    const int rank = CS == 1 ? 0 : (int)(blockIdx.x % CS);
     const int64_t beg = offsets[t], end = offsets[t + 1];
-    const int nchunks = (int)((end - beg + C - 1) / C);
+    const int ntot = (int)((end - beg + C - 1) / C);
+    const int nchunks = ntot > rank ? (ntot - rank + cs - 1) / cs : 0;
+    auto gch = [&](int c) -> int64_t { return (int64_t)c * cs + rank; };
+    float pp[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};   // epilogue: partial predictions (query half x RGB)
 
     if (tid == 0) {
         for (int s = 0; s < STG; ++s) {
@@ -188,7 +211,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // lane g < C owns candidate g of every chunk; its index is loaded two chunks ahead so the
         // dependent idx -> record address load never sits on the chunk's critical path.
         auto load_idx = [&](int c) -> int64_t {
-            const int64_t pos = beg + (int64_t)c * C + lane;
+            const int64_t pos = beg + gch(c) * C + lane;
             return (lane < C && c < nchunks && pos < end) ? (int64_t)__ldg(idx + pos) : 0;
         };
         const int pid = warp == 0 ? 0 : warp - (kEpi0 + kEpiW) + 1;
@@ -197,7 +220,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int64_t e2 = load_idx(c + 2 * kProd);
             const int sl = c % STG;
             if (c >= STG) mbar_wait(&sempty[sl], (uint32_t)((c / STG) - 1) & 1);
-            const int64_t cb = beg + (int64_t)c * C;
+            const int64_t cb = beg + gch(c) * C;
             const int n_in = (int)imin64(C, end - cb);
 #ifdef NDG_TCX_HALFCOPY
             const int n_cp = min(n_in, C / 2);     // knock-out: half the gathers (wrong results)
@@ -266,7 +289,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         for (int c = 0; c < nchunks; ++c) {
             const int sl = c % STG, s = c % kTcStages;
-            const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
+            const int n_in = (int)imin64(C, end - beg - gch(c) * C);
             mbar_wait(&sfull[sl], (uint32_t)(c / STG) & 1);
             if (warp == 2 && lane == 0) NDG_TR(1, c);
             const int as = c % kARing;
@@ -327,12 +350,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         constexpr int NGW = CG;                         // Gaussian slots per warp per item
         constexpr int NLD = (NGW * N + 15) / 16;
         constexpr int NIT = 2;                          // items per chunk
-        float pp[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
         const int g0 = wh * CG;
         const int ngw = wh ? C - CG : CG;
         for (int c = 0; c < nchunks; ++c) {
             const int as = c % kARing;
-            const int n_in = (int)imin64(C, end - beg - (int64_t)c * C);
+            const int n_in = (int)imin64(C, end - beg - gch(c) * C);
 #pragma unroll
             for (int it = 0; it < NIT; ++it) {
                 const int b = it;
@@ -403,6 +425,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) pp[hh][ch] += s_pp[(hh * 128 + q4 * 32 + lane) * 3 + ch];
         }
+        if (cs > 1 && rank > 0 && wh == 0)          // publish this CTA's partials for the cluster's rank 0
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) s_pp[(hh * 128 + q4 * 32 + lane) * 3 + ch] = pp[hh][ch];
+    }
+    if (cs > 1) {
+        cluster_sync();                               // every rank's partials are in its s_pp
+        if (rank == 0 && warp >= kEpi0 && warp < kEpi0 + 4) {
+            const int q4 = warp & 3;
+            for (int r = 1; r < cs; ++r)              // fixed rank order: deterministic sums
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch)
+                        pp[hh][ch] += ld_cluster_f32(&s_pp[(hh * 128 + q4 * 32 + lane) * 3 + ch], r);
+        }
+        cluster_sync();                               // the remote reads are done: ranks > 0 may leave
+    }
+    if (rank == 0 && warp >= kEpi0 && warp < kEpi0 + kEpiW) {
+        const int wh = (warp - kEpi0) >> 2, q4 = warp & 3;
+        constexpr int NIT = 2;
         // tile end: pred, rel-L2 loss, backward query records (group 0 finishes both halves' queries)
         double loss_acc = 0.0;
 #pragma unroll
@@ -440,7 +484,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     tc::fence_before();
     __syncthreads();
-    if (targets && tid == 0) {
+    if (targets && tid == 0 && rank == 0) {
         double sl = 0.0;
         for (int w = 0; w < 8; ++w) sl += s_loss[w];
         loss_partial[t] = sl;
@@ -459,10 +503,31 @@ int launch_forward_tc(int64_t B, int tile, const float* q, const float* tgt, con
     const size_t smem = tc_smem_bytes<N>();
     static DeviceOnce attr;
     if (attr.first()) {
-        cudaFuncSetAttribute(forward_tc_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(forward_tc_kernel<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(forward_tc_kernel<N, kMaxCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
-    forward_tc_kernel<N><<<(unsigned)T, kTcThreads, smem, st>>>(tile, q, tgt, rec_tc, off, idx, eps,
-                                                                1.0 / (3.0 * (double)n_total), pred, qrec, lp);
+    const double inv3n = 1.0 / (3.0 * (double)n_total);
+    // few tiles (T < 148, e.g. cfg1's 64): a cluster of cs CTAs per tile splits its chunks so every SM works
+    const int cs = T * kMaxCluster <= 148 ? kMaxCluster : 1;
+    if (cs == 1) {
+        forward_tc_kernel<N, 1><<<(unsigned)T, kTcThreads, smem, st>>>(tile, q, tgt, rec_tc, off, idx, eps, inv3n, pred,
+                                                                       qrec, lp);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(T * kMaxCluster));
+        cfg.blockDim = dim3(kTcThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)kMaxCluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, forward_tc_kernel<N, kMaxCluster>, tile, q, tgt, rec_tc, off, idx, eps, inv3n, pred,
+                           qrec, lp);
+    }
     NDG_CHECK_LAUNCH();
     return NDG_OK;
 }
