@@ -551,34 +551,42 @@ __global__ void tc_records_kernel(int n, int64_t Gev, const double* __restrict__
     double b = -1.0;                                  // this Gaussian's B_e (< 0: not counted)
     if (e < Gev) {
         const int P = n_chol(n), K = tc_k(n), RT = tc_rec_floats(n);
-        float* out = rec_tc + e * RT;
-        for (int t = 0; t < RT; ++t) out[t] = 0.f;
-        if (eflags[e] & 1) {
-            for (int ch = 0; ch < 3; ++ch) out[n * K + ch] = rec[e * rec_floats(n) + rec_a(n) + ch];   // colour a
-            double L[n_chol(NMAX)], W[n_chol(NMAX)];
+        float4* out4 = reinterpret_cast<float4*>(rec_tc + e * RT);   // RT is a multiple of 4
+        const bool live = eflags[e] & 1;
+        double W[n_chol(NMAX)];
+        if (live) {
+            double L[n_chol(NMAX)];
             for (int t = 0; t < P; ++t) L[t] = chol64[e * P + t];
-            for (int j = 0; j < n; ++j)                     // W = L^-1 (lower), column by column
+            for (int j = 0; j < n; ++j)                 // W = L^-1 (lower), column by column
                 for (int i = j; i < n; ++i) {
                     double acc = (i == j) ? 1.0 : 0.0;
                     for (int k = j; k < i; ++k) acc -= L[tri(i, k)] * W[tri(k, j)];
                     W[tri(i, j)] = acc / L[tri(i, i)];
                 }
-            // plane-major: element (row i, column k) at ((k / 4) * n + i) * 4 + k % 4
-            auto at = [&](int i, int k) -> float& { return out[((k / 4) * n + i) * 4 + (k & 3)]; };
-            double bound = 0.0;
-            for (int i = 0; i < n; ++i) {
-                double bias = 0.0, lin = 0.0;
+        }
+        // plane-major rows: element (row i, column k) at ((k / 4) * n + i) * 4 + k % 4, written as one
+        // 16-B store per (plane, row); columns past the row's diagonal (but the bias at k = n) are 0
+        double bound = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double bias = 0.0, lin = 0.0;
+            float row[NMAX + 8];
+            for (int k = 0; k < K; ++k) row[k] = 0.f;
+            if (live) {
                 for (int j = 0; j <= i; ++j) {
                     const double w = kC * W[tri(i, j)];
-                    at(i, j) = (float)w;
+                    row[j] = (float)w;
                     bias += w * (0.5 - mean64[e * n + j]);
                     lin += fabs(w);
                 }
-                at(i, n) = (float)bias;
+                row[n] = (float)bias;
                 bound = fmax(bound, 0.5 * lin + fabs(bias));
             }
-            if (!(eflags[e] & 2)) b = isfinite(bound) ? bound : 1.0e300;
+            for (int p = 0; p < K / 4; ++p)
+                out4[p * n + i] = make_float4(row[4 * p], row[4 * p + 1], row[4 * p + 2], row[4 * p + 3]);
         }
+        const float* ra = rec + e * rec_floats(n) + rec_a(n);
+        out4[n * K / 4] = live ? make_float4(ra[0], ra[1], ra[2], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);   // colour a
+        if (live && !(eflags[e] & 2)) b = isfinite(bound) ? bound : 1.0e300;
     }
     if (cond) {
         // warp-reduce [max, sum of squares, count] first: one set of atomics per warp, not per Gaussian
