@@ -175,3 +175,19 @@ def test_frozen_rows_are_compacted_and_checkpointed_in_place(cuda, tmp_path):
     half, phalf = run(40)
     resumed, pres = run(80, resume_from=phalf)
     assert pres.read_bytes() == pfull.read_bytes()
+
+
+@pytest.mark.parametrize("target", ["gmm", "shading"])
+def test_graphed_fit_equals_eager_fit(cuda, target):
+    """TrainConfig.graph replays the captured step (GraphedStep, re-captured after every refinement event;
+    the gmm target through GraphedEval); the fit is bit-identical to the eager loop's."""
+    D, T = _T()
+    out = {}
+    for graph in (True, False):
+        tgt = D.GmmOracleTarget(1, 6, 8) if target == "gmm" else D.ShadingToyTarget(1, 6)
+        cfg = T.TrainConfig(iterations=90, phase_length=30, warmup_phases=1, n_components=40, batch_size=2048,
+                            seed=3, graph=graph)
+        res = T.train(cfg, tgt, 6)
+        out[graph] = (res.mixture.params.clone(), [m.loss for m in res.metrics], len(res.events))
+    assert torch.equal(out[True][0], out[False][0])
+    assert out[True][1] == out[False][1] and out[True][2] == out[False][2] == 3
