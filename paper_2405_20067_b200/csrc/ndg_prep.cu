@@ -757,7 +757,8 @@ __device__ void solve_upper_t(int n, const double* L, const double* Y, double* X
         }
 }
 
-__global__ void epilogue_kernel(int n, int64_t G, int64_t Gev, int amp_mode, const float* __restrict__ params,
+// One thread per component (large G: enough components to fill the GPU; see epilogue_kernel).
+__global__ void epilogue_thread_kernel(int n, int64_t G, int64_t Gev, int amp_mode, const float* __restrict__ params,
                                 const float* __restrict__ child, const uint8_t* __restrict__ flags,
                                 const uint8_t* __restrict__ eflags, const double* __restrict__ chol64,
                                 const double* __restrict__ accum, float* __restrict__ gp, float* __restrict__ gc,
@@ -858,6 +859,155 @@ __global__ void epilogue_kernel(int n, int64_t G, int64_t Gev, int amp_mode, con
     }
 }
 
+// Warp per component, for small G (cfg1: 4096 components are 128 one-thread-per-component warps): lane c
+// runs column c of X = L^-T S (back substitution), and the P-entry and n-entry loops of the chain rule are
+// spread over the lanes; the matrices live in the warp's slice of shared memory. Every value is computed in
+// the same order as in epilogue_thread_kernel, so the two give the same bits. At 100k components the warp
+// form is issue-bound on its lane-serial parts (436 vs 393 us), so large G keeps one thread per component.
+constexpr int kEpiWarps = 8;
+constexpr int64_t kEpiWarpMaxG = 16384;   // the warp form up to here (cfg1 4096: 37 -> ~20 us), threads beyond
+
+__host__ __device__ constexpr int epi_doubles(int n) { return 3 * n_chol(n) + 2 * n * n + 2 * n; }   // per warp
+
+__device__ __forceinline__ void tri_rc(int t, int& r, int& c) {   // packed lower index -> (row, col)
+    r = (int)((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);
+    r += (r + 1) * (r + 2) / 2 <= t;
+    r -= r * (r + 1) / 2 > t;
+    c = t - r * (r + 1) / 2;
+}
+
+__global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(
+    int n, int64_t G, int64_t Gev, int amp_mode, const float* __restrict__ params, const float* __restrict__ child,
+    const uint8_t* __restrict__ flags, const uint8_t* __restrict__ eflags, const double* __restrict__ chol64,
+    const double* __restrict__ accum, float* __restrict__ gp, float* __restrict__ gc, float* __restrict__ stats,
+    ndg_status* st) {
+    extern __shared__ double esm[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int P = n_chol(n), R = raw_floats(n), A = acc_doubles(n), nn = n * n;
+    double* sLp = esm + wib * epi_doubles(n);   // the parent's L (packed)
+    double* sL = sLp + P;                       // L of the evaluated Gaussian e (packed)
+    double* sU = sL + P;                        // the child's activated U (packed)
+    double* sGL = sU + P;                       // X = L^-T S, then G_L = -tril(X) of e (dense n x n)
+    double* sGLp = sGL + nn;                    // accumulated parent G_L (dense)
+    double* sdm = sGLp + nn;                    // dm of e
+    double* sdmp = sdm + n;                     // accumulated parent dm
+    const int64_t i = blockIdx.x * (int64_t)kEpiWarps + wib;
+    if (i >= G) return;                         // warp-uniform
+    const double invC = 1.0 / kC, invC2 = invC * invC;
+    float* op = gp + i * R;
+    float* oc = gc ? gc + i * R : nullptr;
+    for (int t = lane; t < R; t += 32) {
+        op[t] = 0.f;
+        if (oc) oc[t] = 0.f;
+    }
+    for (int t = lane; t < P; t += 32) sLp[t] = chol64[i * P + t];
+    for (int t = lane; t < nn; t += 32) sGLp[t] = 0.0;
+    for (int t = lane; t < n; t += 32) sdmp[t] = 0.0;
+    const int nev = (Gev == 2 * G) ? 2 : 1;
+    for (int which = 0; which < nev; ++which) {
+        const int64_t e = which ? G + i : i;
+        const double* acc = accum + e * A;
+        float* so = stats + e * kNumStats;
+        if (!(eflags[e] & 1)) {                 // warp-uniform
+            if (lane == 0) so[0] = so[1] = so[2] = 0.f;
+            continue;
+        }
+        if (lane == 0) {
+            so[0] = (float)acc[acc_tail(n) + 3];
+            so[1] = (float)(acc[acc_tail(n) + 4] * invC);
+            so[2] = (float)acc[acc_tail(n) + 5];
+        }
+        for (int t = lane; t < P; t += 32) sL[t] = chol64[e * P + t];
+        __syncwarp();
+        if (lane < n) {                         // X[:, c] = L^-T S[:, c], S = -sym(S') / C^2
+            const int c = lane;
+            for (int r = n - 1; r >= 0; --r) {
+                double a = -acc[r >= c ? tri(r, c) : tri(c, r)] * invC2;
+                for (int k = r + 1; k < n; ++k) a -= sL[tri(k, r)] * sGL[k * n + c];
+                sGL[r * n + c] = a / sL[tri(r, r)];
+            }
+        }
+        __syncwarp();
+        for (int t = lane; t < nn; t += 32) {
+            const int r = t / n, c = t - (t / n) * n;
+            sGL[t] = c <= r ? -sGL[t] : 0.0;
+        }
+        if (lane == 0) {                        // dm = -L^-T t (single-column back substitution)
+            for (int r = n - 1; r >= 0; --r) {
+                double a = -acc[P + r] * invC;
+                for (int k = r + 1; k < n; ++k) a -= sL[tri(k, r)] * sdm[k];
+                sdm[r] = a / sL[tri(r, r)];
+            }
+            for (int r = 0; r < n; ++r) sdm[r] = -sdm[r];
+        }
+        const float* row = which ? child + i * R : params + i * R;
+        float* out = which ? oc : op;
+        if (lane == 0) {                        // colour and amplitude
+            const double ar = (double)row[n + P + 3];
+            const double alpha = amp_mode == NDG_BRIGHTNESS ? exp(ar) : sigmoid64(ar);
+            double dalpha = 0.0;
+            for (int ch = 0; ch < 3; ++ch) {
+                const double cc = sigmoid64((double)row[n + P + ch]);
+                const double gA = acc[acc_tail(n) + ch];
+                out[n + P + ch] = (float)(gA * alpha * cc * (1.0 - cc));
+                dalpha += gA * cc;
+            }
+            out[n + P + 3] = (float)(dalpha * (amp_mode == NDG_BRIGHTNESS ? alpha : alpha * (1.0 - alpha)));
+        }
+        __syncwarp();
+        if (!which) {
+            for (int t = lane; t < nn; t += 32) sGLp[t] += sGL[t];
+            for (int r = lane; r < n; r += 32) sdmp[r] += sdm[r];
+        } else {
+            const float* crow = child + i * R;
+            for (int t = lane; t < P; t += 32) {
+                int r, c;
+                tri_rc(t, r, c);
+                const double raw = (double)crow[n + t];
+                sU[t] = (r == c) ? exp(raw) : act_offdiag(raw);
+            }
+            __syncwarp();
+            for (int t = lane; t < P; t += 32) {
+                int r, c;
+                tri_rc(t, r, c);
+                double s1 = 0.0, s2 = 0.0;
+                for (int k = 0; k <= c; ++k) s1 += sGL[r * n + k] * sU[tri(c, k)];     // (G U^T)_rc
+                for (int k = r; k < n; ++k) s2 += sLp[tri(k, r)] * sGL[k * n + c];    // (L^T G)_rc
+                sGLp[r * n + c] += s1 + sdm[r] * (double)crow[c];
+                const double d = s2 * (r == c ? sU[tri(r, r)] : (1.0 - sU[tri(r, c)] * sU[tri(r, c)]) * 0.5);
+                out[n + t] = (float)d;
+            }
+            for (int r = lane; r < n; r += 32) {
+                double s = 0.0;
+                for (int k = r; k < n; ++k) s += sLp[tri(k, r)] * sdm[k];
+                out[r] = (float)s;
+                sdmp[r] += sdm[r];
+            }
+        }
+        __syncwarp();
+    }
+    for (int r = lane; r < n; r += 32) op[r] = (float)sdmp[r];
+    for (int t = lane; t < P; t += 32) {
+        int r, c;
+        tri_rc(t, r, c);
+        const double l = sLp[t];
+        op[n + t] = (float)(sGLp[r * n + c] * (r == c ? l : (1.0 - l * l) * 0.5));
+    }
+    __syncwarp();
+    // non-finite gradient -> NonFiniteGradientError: the lowest offending entry of each row
+    for (int which = 0; which < nev; ++which) {
+        const float* out = which ? oc : op;
+        for (int base = 0; base < R; base += 32) {
+            const int t = base + lane;
+            const unsigned m = __ballot_sync(0xffffffffu, t < R && !isfinite(out[t]));
+            if (m) {
+                if (lane == 0) record_key(&st->nonfinite_key, (which ? G * R : 0) + i * R + base + __ffs(m) - 1);
+                break;
+            }
+        }
+    }
+}
+
 extern "C" int ndg_epilogue(int n, int64_t G, int64_t Gev, int amp_mode, const float* params, const float* child,
                             const uint8_t* flags, const uint8_t* eflags, const double* chol64, const double* accum,
                             float* grad_params, float* grad_child, float* stats, ndg_status* status, void* stream) {
@@ -865,8 +1015,19 @@ extern "C" int ndg_epilogue(int n, int64_t G, int64_t Gev, int amp_mode, const f
     NDG_REQUIRE(Gev == G || Gev == 2 * G, "Gev must be G or 2G");
     NDG_REQUIRE(Gev == G || (child && grad_child), "child rows and child gradients required when Gev == 2G");
     if (G == 0) return NDG_OK;
-    const int threads = spread_threads(G, 64);
-    epilogue_kernel<<<(unsigned)((G + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+    if (G > kEpiWarpMaxG) {
+        const int threads = 64;
+        epilogue_thread_kernel<<<(unsigned)((G + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+            n, G, Gev, amp_mode, params, child, flags, eflags, chol64, accum, grad_params,
+            Gev == 2 * G ? grad_child : nullptr, stats, status);
+        NDG_CHECK_LAUNCH();
+        return NDG_OK;
+    }
+    const size_t smem = sizeof(double) * kEpiWarps * epi_doubles(n);
+    static DeviceOnce attr;
+    if (attr.first())
+        cudaFuncSetAttribute(epilogue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    epilogue_kernel<<<(unsigned)((G + kEpiWarps - 1) / kEpiWarps), kEpiWarps * 32, smem, as_stream(stream)>>>(
         n, G, Gev, amp_mode, params, child, flags, eflags, chol64, accum, grad_params,
         Gev == 2 * G ? grad_child : nullptr, stats, status);
     NDG_CHECK_LAUNCH();
