@@ -10,6 +10,7 @@
 #include <cstring>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ndg_common.cuh"
 
@@ -1015,7 +1016,12 @@ extern "C" int ndg_epilogue(int n, int64_t G, int64_t Gev, int amp_mode, const f
     NDG_REQUIRE(Gev == G || Gev == 2 * G, "Gev must be G or 2G");
     NDG_REQUIRE(Gev == G || (child && grad_child), "child rows and child gradients required when Gev == 2G");
     if (G == 0) return NDG_OK;
-    if (G > kEpiWarpMaxG) {
+    // NDG_EPILOGUE_WARP_MAX overrides the crossover (tests pin the two forms against each other)
+    static const int64_t warp_max = [] {
+        const char* v = getenv("NDG_EPILOGUE_WARP_MAX");
+        return v ? (int64_t)atoll(v) : kEpiWarpMaxG;
+    }();
+    if (G > warp_max) {
         const int threads = 64;
         epilogue_thread_kernel<<<(unsigned)((G + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
             n, G, Gev, amp_mode, params, child, flags, eflags, chol64, accum, grad_params,

@@ -63,3 +63,29 @@ def test_far_gaussian_contributes_exact_zero(cuda):
     assert np.all(g[1] == 0.0) and np.any(g[0] != 0.0)
     ref = O.fwd_bwd(om, q, t, hp.ps.vectors)
     assert np.linalg.norm(g[0] - ref["grad_parent"][0]) <= 1e-4 * np.linalg.norm(ref["grad_parent"][0])
+
+
+def test_epilogue_warp_and_thread_forms_agree_bitwise(cuda, tmp_path):
+    """K8 runs a warp per component for small G and a thread per component for large G
+    (NDG_EPILOGUE_WARP_MAX); both evaluate the same operations in the same order, so a step's gradients
+    are byte-identical whichever form ran (checked in two processes, one per form)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import paper_2405_20067_b200 as ndg\n"
+        "from oracle import ndg_oracle as O\n"
+        "om, _ = O.synthetic_mixture(7, 300, seed=5, children=True)\n"
+        "mix = ndg.Mixture.from_arrays(7, om.amp_mode, om.params, om.child, om.has_child, om.frozen)\n"
+        "q = torch.from_numpy(O.synthetic_queries(7, 1024, seed=6)).cuda()\n"
+        "t = torch.from_numpy(O.synthetic_targets(1024, seed=7)).cuda()\n"
+        "r = ndg.HotPath(7, projection_seed=2).fwd_bwd(mix, q, t)\n"
+        "np.save(sys.argv[1], r.grads.flat.cpu().numpy())\n" % root)
+    outs = []
+    for tag, env in (("warp", {}), ("thread", {"NDG_EPILOGUE_WARP_MAX": "0"})):
+        path = tmp_path / f"{tag}.npy"
+        subprocess.check_call([sys.executable, "-c", code, str(path)], env=dict(os.environ, **env))
+        outs.append(np.load(path))
+    assert outs[0].tobytes() == outs[1].tobytes()
