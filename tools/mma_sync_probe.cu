@@ -1,5 +1,6 @@
-// mma.sync m16n8k8 tf32 throughput probe (sm_100a): is the legacy warp-level MMA fast enough to carry
-// the N >= 13 backward's S = Z^T W Z accumulation in registers?
+// mma.sync throughput probe (sm_100a): m16n8k8 tf32 (round 1: is the legacy warp-level MMA fast enough to
+// carry the N >= 13 backward's S = Z^T W Z accumulation in registers?) and m16n8k16 f16 (round 2: it
+// issues at the same 0.467 MMA/clk/SM with twice the K, which K7-MMA now uses).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_sync_probe tools/mma_sync_probe.cu
 #include <cstdio>
 #include <cuda_runtime.h>
