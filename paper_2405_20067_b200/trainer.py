@@ -26,7 +26,7 @@ import torch
 
 from . import datasets as D
 from .engine import GraphedStep, HotPath, adam_step, new_adam_state
-from .errors import TrainingAborted
+from .errors import NonFiniteGradientError, TrainingAborted
 from .gmm import BRIGHTNESS, FLAG_CHILD, FLAG_FROZEN, Mixture, n_chol, raw_slices, raw_width, tri
 
 
@@ -157,11 +157,20 @@ class Trainer:
     def iteration(self) -> MetricsRow:
         cfg = self.cfg
         t0 = time.perf_counter()
-        res = self._step()
+        try:
+            res = self._step()
+        except NonFiniteGradientError as err:                       # a training abort
+            self.mix = self.last_good.clone()
+            self._gs = None
+            raise TrainingAborted(f"non-finite gradient at iteration {self.step_no} ({self._batch_name()}; "
+                                  f"component {err.component}, block {err.block}, batch index {err.batch_index})",
+                                  iteration=self.step_no) from err
         self.last_allreduce_bytes = res.grads.reduced().numel() * 4 if self.allreduce is not None else 0
         if not math.isfinite(res.loss):
             self.mix = self.last_good.clone()
-            raise TrainingAborted(f"non-finite loss at iteration {self.step_no}", iteration=self.step_no)
+            self._gs = None
+            raise TrainingAborted(f"non-finite loss at iteration {self.step_no} ({self._batch_name()})",
+                                  iteration=self.step_no)
         self.step_no += 1
         st = res.grads.stats.double()
         if self.phase_stats is None or self.phase_stats.shape != st.shape:
@@ -177,6 +186,13 @@ class Trainer:
         self.low_count = torch.where(low, self.low_count + 1, torch.zeros_like(self.low_count))
         ms = (time.perf_counter() - t0) * 1e3
         return MetricsRow(self.step_no, res.loss, int(self.live_components()), 1.0 - res.kept_fraction, ms)
+
+    def _batch_name(self) -> str:
+        """The offending batch of an abort: the state that regenerates it."""
+        if isinstance(self.target, D.FileDataset):
+            st = self.target.state()
+            return f"file batch {st['draw'] - 1}, epoch {st['epoch']}"
+        return f"batch draw {self.sampler.draw - 1} of sampler seed {self.sampler.seed}"
 
     def _step(self):
         """sample_batch + fwd_bwd (+ the allreduce). Small working sets (worst-case candidate list <= 2^24)

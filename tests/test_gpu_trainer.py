@@ -191,3 +191,38 @@ def test_graphed_fit_equals_eager_fit(cuda, target):
         out[graph] = (res.mixture.params.clone(), [m.loss for m in res.metrics], len(res.events))
     assert torch.equal(out[True][0], out[False][0])
     assert out[True][1] == out[False][1] and out[True][2] == out[False][2] == 3
+
+
+def test_non_finite_loss_aborts_with_last_good_mixture(cuda, tmp_path):
+    """a non-finite loss aborts the fit (TrainingAborted naming the iteration and the
+    batch) with the last good mixture; `ndgauss fit` then writes that checkpoint and exits 3."""
+    from paper_2405_20067_b200 import cli
+    from paper_2405_20067_b200 import errors as E
+    from paper_2405_20067_b200 import formats as F
+    D, T = _T()
+    inner = D.ShadingToyTarget(0, 6)
+    calls = [0]
+
+    def bad_target(q):                       # finite for 5 batches, then NaN targets
+        calls[0] += 1
+        out = inner(q)
+        return out if calls[0] <= 5 else out * float("nan")
+    cfg = T.TrainConfig(iterations=20, n_components=32, batch_size=1024, seed=1)
+    tr = T.Trainer(cfg, bad_target, 6)
+    p0 = tr.mix.params.clone()
+    with pytest.raises(E.TrainingAborted) as ei:
+        for _ in range(cfg.iterations):
+            tr.iteration()
+    assert ei.value.iteration == 5 and "batch draw" in str(ei.value)
+    assert torch.equal(tr.mix.params, p0)                          # last good = the initial mixture
+    # the CLI: a tensor file whose targets turn NaN part-way
+    q = np.random.default_rng(0).random((4096, 6), dtype=np.float32)
+    t = np.random.default_rng(1).random((4096, 3), dtype=np.float32)
+    t[2000:] = np.nan
+    path = tmp_path / "bad.ndgt"
+    F.write_ndgt(path, q, t)
+    c = tmp_path / "c.cfg"
+    c.write_text(f"[trainer]\niterations = 30\nn_components = 32\nbatch_size = 1024\n[data]\ntarget = file\n"
+                 f"path = {path}\nn_dims = 6\n")
+    assert cli.main(["fit", "--config", str(c), "--out", str(tmp_path / "o")]) == 3
+    assert (tmp_path / "o" / "checkpoint.ndgc").exists()
