@@ -226,3 +226,28 @@ def test_non_finite_loss_aborts_with_last_good_mixture(cuda, tmp_path):
                  f"path = {path}\nn_dims = 6\n")
     assert cli.main(["fit", "--config", str(c), "--out", str(tmp_path / "o")]) == 3
     assert (tmp_path / "o" / "checkpoint.ndgc").exists()
+
+
+@pytest.mark.parametrize("n_dims", [3, 4])
+def test_single_gaussian_recovery(cuda, n_dims):
+    """SPEC.md:332 example: a single-Gaussian target fitted by a single-component mixture for 2000
+    iterations reaches held-out relative L2 below 1e-3 (target sigma 0.3 -- the SPEC leaves the target's
+    width open; at sigma 0.15 in N >= 3 most uniform queries see a numerically zero target and the fit can
+    settle on the zero function, which the eps-regularised loss barely penalises)."""
+    D, T = _T()
+    tgt = D.GmmOracleTarget(7, n_dims, 1, sigma0=0.3)
+    cfg = T.TrainConfig(iterations=2000, phase_length=10 ** 6, n_components=1, batch_size=4096, seed=1)
+    res = T.train(cfg, tgt, n_dims)
+    assert T.held_out_rel_l2(res.mixture, tgt, n_dims) < 1e-3
+
+
+def test_cli_fit_zero_iterations(cuda, tmp_path):
+    """iterations = 0 writes the initial checkpoint and a metrics.csv with only its header,
+    exit 0."""
+    from paper_2405_20067_b200 import cli
+    c = tmp_path / "c.cfg"
+    c.write_text("[trainer]\niterations = 0\nn_components = 16\nbatch_size = 1024\n[data]\ntarget = gmm\nn_dims = 4\n")
+    assert cli.main(["fit", "--config", str(c), "--out", str(tmp_path / "o")]) == 0
+    assert (tmp_path / "o" / "checkpoint.ndgc").exists()
+    assert (tmp_path / "o" / "metrics.csv").read_text().splitlines() == [
+        "iteration,loss,n_components,culled_fraction,ms_per_iter"]
