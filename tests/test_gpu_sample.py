@@ -89,3 +89,44 @@ def test_sorted_tiling_culls_at_least_random_tiling(cuda):
         for qq, acc in ((q, kept_sorted), (q[perm].contiguous(), kept_random)):
             acc.append(hp.cull(hp.tile_bounds(qq), pb).kept_fraction(recs.Gev))
     assert np.mean(kept_sorted) <= np.mean(kept_random), (np.mean(kept_sorted), np.mean(kept_random))
+
+
+def test_gmm_target_spec_examples(cuda):
+    """one component queried at its mean gives alpha * c exactly (to float32); the same
+    seed twice gives identical targets; sample_batch with batch_size = tile_size is one tile."""
+    D = _D()
+    tgt = D.GmmOracleTarget(3, 5, 1)
+    row = tgt.mixture.params[0].double().cpu().numpy()
+    mean = torch.tensor(row[:5], dtype=torch.float32, device="cuda")
+    q = mean.repeat(256, 1).contiguous()
+    got = tgt(q)[0].double().cpu().numpy()
+    n, P = 5, 15
+    color = 1.0 / (1.0 + np.exp(-row[n + P:n + P + 3]))
+    alpha = np.exp(row[n + P + 3])
+    assert np.allclose(got, alpha * color, rtol=1e-6, atol=0)
+    a = D.GmmOracleTarget(11, 6, 4)(D.QuerySampler(1).queries(6, 1024, 256, "cuda"))
+    b = D.GmmOracleTarget(11, 6, 4)(D.QuerySampler(1).queries(6, 1024, 256, "cuda"))
+    assert torch.equal(a, b)
+    q1, t1 = D.sample_batch(tgt, 5, 256, 256, D.QuerySampler(2), "cuda")
+    assert q1.shape == (256, 5) and t1.shape == (256, 3) and torch.all(q1[1:, 0] >= q1[:-1, 0])
+
+
+def test_shading_toy_spec_examples(cuda):
+    """the glossy lobe's exponent is at its minimum at roughness 1 (the broadest lobe: for
+    the same view / reflection alignment the glossy term is largest), and a grid slice equals the
+    generator evaluated pointwise (the kernel against the float64 restatement, per query)."""
+    D = _D()
+    tgt = D.ShadingToyTarget(5, 10)
+    q = D.QuerySampler(3).queries(10, 4096, 256, "cuda")
+    lo, hi = q.clone(), q.clone()
+    lo[:, 9], hi[:, 9] = 0.0, 1.0
+    lo[:, 6:9] = hi[:, 6:9] = 0.0                          # albedo 0: only the glossy term 0.4 * lobe remains
+    glossy0, glossy1 = tgt(lo).double().cpu().numpy(), tgt(hi).double().cpu().numpy()
+    assert np.all(glossy1 >= glossy0 - 1e-7) and glossy1.mean() > glossy0.mean()
+    u = torch.linspace(0, 1, 64, device="cuda")
+    grid = torch.full((64 * 64, 10), 0.5, device="cuda")
+    grid[:, 0] = u.repeat_interleave(64)
+    grid[:, 1] = u.repeat(64)
+    img = tgt(grid).double().cpu().numpy()
+    ref = O.shading_toy(grid.cpu().numpy(), tgt.freq, tgt.phase)
+    assert np.max(np.abs(img - ref)) < 2e-5
