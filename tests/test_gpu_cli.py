@@ -86,3 +86,29 @@ def test_gradcheck_command(cuda):
     assert cli.main(["gradcheck", "--seed", "3", "--per-n", "2", "--fp32"]) == 0
     assert not gradcheck.run(seed=3, per_n=1, dims=(4,), corrupt=True, out=lambda *_: None)
     assert not gradcheck.run(seed=3, per_n=1, dims=(4,), corrupt=True, out=lambda *_: None, analytic="fp32")
+
+
+def test_cli_spec_examples(cuda, tmp_path):
+    """a fixed-seed gmm-oracle fit run twice writes the same metrics.csv (every column
+    but the wall-clock ms_per_iter); eval of an empty query file writes an empty output and exits 0; a
+    query file of the wrong dimension exits 2."""
+    from paper_2405_20067_b200 import cli
+    from paper_2405_20067_b200 import formats as F
+    cfgp = tmp_path / "fit.cfg"
+    cfgp.write_text("[trainer]\niterations = 30\nphase_length = 15\nbatch_size = 2048\nn_components = 32\nseed = 4\n"
+                    "[data]\ntarget = gmm\nn_dims = 4\ntarget_components = 4\n")
+    runs = []
+    for k in range(2):
+        out = tmp_path / f"r{k}"
+        assert cli.main(["fit", "--config", str(cfgp), "--out", str(out)]) == 0
+        runs.append([r.rsplit(",", 1)[0] for r in (out / "metrics.csv").read_text().splitlines()])
+    assert runs[0] == runs[1] and len(runs[0]) == 31
+    ck = tmp_path / "r0" / "checkpoint.ndgc"
+    F.write_ndgt(tmp_path / "empty.ndgt", np.zeros((0, 4), np.float32), np.zeros((0, 3), np.float32))
+    assert cli.main(["eval", "--ckpt", str(ck), "--queries", str(tmp_path / "empty.ndgt"), "--out",
+                     str(tmp_path / "e0")]) == 0
+    q, p, _ = F.read_ndgt(tmp_path / "e0" / "pred.ndgt")
+    assert q.shape == (0, 4) and p.shape == (0, 3)
+    F.write_ndgt(tmp_path / "q5.ndgt", np.zeros((8, 5), np.float32), np.zeros((8, 3), np.float32))
+    assert cli.main(["eval", "--ckpt", str(ck), "--queries", str(tmp_path / "q5.ndgt"), "--out",
+                     str(tmp_path / "e1")]) == 2
