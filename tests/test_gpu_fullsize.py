@@ -33,6 +33,7 @@ CASES = [
     ("cfg2-R-children-frozen", 10, 100_000, 1 << 20, "R", 4, True, 0, 0.1),
     ("cfg4-R", 16, 500_000, 1 << 22, "R", 1, False, 0, 0.0),
     ("cfg4-C", 16, 500_000, 1 << 22, "C", 2, False, 0, 0.0),
+    ("cfg4-C-children-opacity", 16, 500_000, 1 << 22, "C", 2, True, 1, 0.0),   # K7-MMA over Gev = 1M
     ("cfg5-R", 10, 1_000_000, 1 << 19, "R", 1, False, 0, 0.0),
     ("cfg5-C-children", 10, 1_000_000, 1 << 19, "C", 8, True, 0, 0.0),
 ]
