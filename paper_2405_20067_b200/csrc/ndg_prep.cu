@@ -749,26 +749,23 @@ extern "C" int ndg_loss_finalize(int64_t T, const double* loss_partial, double* 
 //          parent += tril(G_Lc U^T) + tril(dm_c m_u^T) on L and dm_c on the mean.
 //   colour / amplitude: d color_raw = gA * alpha * c (1 - c); d amp_raw = (gA . c) * alpha'.
 // ---------------------------------------------------------------------------------------------
-__device__ void solve_upper_t(int n, const double* L, const double* Y, double* X) {   // X = L^-T Y (dense N x N)
-    for (int c = 0; c < n; ++c)
-        for (int i = n - 1; i >= 0; --i) {
-            double acc = Y[i * n + c];
-            for (int k = i + 1; k < n; ++k) acc -= L[tri(k, i)] * X[k * n + c];
-            X[i * n + c] = acc / L[tri(i, i)];
-        }
-}
 
-// One thread per component (large G: enough components to fill the GPU; see epilogue_kernel).
-__global__ void epilogue_thread_kernel(int n, int64_t G, int64_t Gev, int amp_mode, const float* __restrict__ params,
-                                const float* __restrict__ child, const uint8_t* __restrict__ flags,
-                                const uint8_t* __restrict__ eflags, const double* __restrict__ chol64,
-                                const double* __restrict__ accum, float* __restrict__ gp, float* __restrict__ gc,
-                                float* __restrict__ stats, ndg_status* st) {
+// One thread per component (large G: enough components to fill the GPU; see epilogue_kernel). Templated on
+// N with the solve done in place (S -> X -> G_L in one N x N array), so its float64 scratch is 2 N^2 + P + 2N
+// doubles instead of 4 x 16^2 + 136 + 32 (the local-memory traffic that made it DRAM-bound: 1 GB at 100k
+// components). Same operations in the same order as before, so the same bits.
+template <int N>
+__global__ void epilogue_thread_kernel(int64_t G, int64_t Gev, int amp_mode, const float* __restrict__ params,
+                                       const float* __restrict__ child, const uint8_t* __restrict__ flags,
+                                       const uint8_t* __restrict__ eflags, const double* __restrict__ chol64,
+                                       const double* __restrict__ accum, float* __restrict__ gp,
+                                       float* __restrict__ gc, float* __restrict__ stats, ndg_status* st) {
+    constexpr int n = N;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= G) return;
-    const int P = n_chol(n), R = raw_floats(n), A = acc_doubles(n);
-    double GLp[NMAX * NMAX], dmp[NMAX];
-    double S[NMAX * NMAX], X[NMAX * NMAX];
+    constexpr int P = n_chol(N), R = raw_floats(N), A = acc_doubles(N);
+    double GLp[N * N], dmp[N];
+    double X[N * N];                     // S, then X = L^-T S in place, then G_L = -tril(X) in place
     for (int t = 0; t < n * n; ++t) GLp[t] = 0.0;
     for (int r = 0; r < n; ++r) dmp[r] = 0.0;
     float* op = gp + i * R;
@@ -792,11 +789,17 @@ __global__ void epilogue_thread_kernel(int n, int64_t G, int64_t Gev, int amp_mo
         so[2] = (float)acc[acc_tail(n) + 5];
         const double* Le = chol64 + e * P;
         for (int r = 0; r < n; ++r)
-            for (int c = 0; c <= r; ++c) S[r * n + c] = S[c * n + r] = -acc[tri(r, c)] * invC2;
-        solve_upper_t(n, Le, S, X);
-        double GL[NMAX * NMAX], dm[NMAX];
+            for (int c = 0; c <= r; ++c) X[r * n + c] = X[c * n + r] = -acc[tri(r, c)] * invC2;
+        for (int c = 0; c < n; ++c)                      // X = L^-T S, column c, rows n-1 .. 0, in place
+            for (int r = n - 1; r >= 0; --r) {
+                double a = X[r * n + c];
+                for (int k = r + 1; k < n; ++k) a -= Le[tri(k, r)] * X[k * n + c];
+                X[r * n + c] = a / Le[tri(r, r)];
+            }
+        double* GL = X;
         for (int r = 0; r < n; ++r)
             for (int c = 0; c < n; ++c) GL[r * n + c] = c <= r ? -X[r * n + c] : 0.0;
+        double dm[N];
         for (int r = n - 1; r >= 0; --r) {   // dm = -L^-T t (single-column back substitution)
             double a = -acc[P + r] * invC;
             for (int k = r + 1; k < n; ++k) a -= Le[tri(k, r)] * dm[k];
@@ -820,7 +823,7 @@ __global__ void epilogue_thread_kernel(int n, int64_t G, int64_t Gev, int amp_mo
             for (int r = 0; r < n; ++r) dmp[r] += dm[r];
         } else {
             const float* crow = child + i * R;
-            double U[n_chol(NMAX)];
+            double U[P];
             for (int r = 0; r < n; ++r)
                 for (int c = 0; c <= r; ++c) {
                     const double raw = (double)crow[n + tri(r, c)];
@@ -864,7 +867,7 @@ __global__ void epilogue_thread_kernel(int n, int64_t G, int64_t Gev, int amp_mo
 // runs column c of X = L^-T S (back substitution), and the P-entry and n-entry loops of the chain rule are
 // spread over the lanes; the matrices live in the warp's slice of shared memory. Every value is computed in
 // the same order as in epilogue_thread_kernel, so the two give the same bits. At 100k components the warp
-// form is issue-bound on its lane-serial parts (436 vs 393 us), so large G keeps one thread per component.
+// form is issue-bound on its lane-serial parts (436 vs 348 us), so large G keeps one thread per component.
 constexpr int kEpiWarps = 8;
 constexpr int64_t kEpiWarpMaxG = 16384;   // the warp form up to here (cfg1 4096: 37 -> ~20 us), threads beyond
 
@@ -1023,9 +1026,19 @@ extern "C" int ndg_epilogue(int n, int64_t G, int64_t Gev, int amp_mode, const f
     }();
     if (G > warp_max) {
         const int threads = 64;
-        epilogue_thread_kernel<<<(unsigned)((G + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
-            n, G, Gev, amp_mode, params, child, flags, eflags, chol64, accum, grad_params,
-            Gev == 2 * G ? grad_child : nullptr, stats, status);
+        const unsigned grid = (unsigned)((G + threads - 1) / threads);
+        float* gch = Gev == 2 * G ? grad_child : nullptr;
+        switch (n) {
+#define NDG_CASE(NN)                                                                                      \
+    case NN:                                                                                              \
+        epilogue_thread_kernel<NN><<<grid, threads, 0, as_stream(stream)>>>(G, Gev, amp_mode, params, child, \
+                                                                           flags, eflags, chol64, accum,  \
+                                                                           grad_params, gch, stats, status); \
+        break;
+            NDG_CASE(1) NDG_CASE(2) NDG_CASE(3) NDG_CASE(4) NDG_CASE(5) NDG_CASE(6) NDG_CASE(7) NDG_CASE(8)
+            NDG_CASE(9) NDG_CASE(10) NDG_CASE(11) NDG_CASE(12) NDG_CASE(13) NDG_CASE(14) NDG_CASE(15) NDG_CASE(16)
+#undef NDG_CASE
+        }
         NDG_CHECK_LAUNCH();
         return NDG_OK;
     }
