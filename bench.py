@@ -432,12 +432,13 @@ def run_regime(a, regime, torch, ndg, D, K, dist, rank, world, dev, steps, warmu
 def our_arm(a, rank, world):
     import torch
     dist = None
+    # bind the rank's GPU before the process group, so NCCL's communicator and barriers use it
+    local = int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
         # NDG_DIST_BACKEND=gloo only for plumbing checks with several ranks on one GPU (NCCL refuses that)
         dist.init_process_group(os.environ.get("NDG_DIST_BACKEND", "nccl"))
-    local = int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2405_20067_b200 as ndg
     from paper_2405_20067_b200 import datasets as D
