@@ -270,6 +270,12 @@ int ndg_epilogue(int n, int64_t G, int64_t Gev, int amp_mode, const float* param
 int ndg_adam(int n, int64_t rows, float* params, const float* grad, float* m1, float* m2, const uint8_t* row_mask,
              int step, float lr_mean, float lr_chol, float lr_color, float lr_amp, float beta1, float beta2,
              float eps, void* stream);
+/* K9 with the row selection taken from the mixture's flag bytes (bit0 live child, bit1 frozen): row r is
+ * updated iff (flags[r] & require) == require and (flags[r] & forbid) == 0 -- parents: require 0, forbid
+ * frozen; live children: require child, forbid frozen. Same arithmetic as ndg_adam. */
+int ndg_adam_flags(int n, int64_t rows, float* params, const float* grad, float* m1, float* m2, const uint8_t* flags,
+                   int require, int forbid, int step, float lr_mean, float lr_chol, float lr_color, float lr_amp,
+                   float beta1, float beta2, float eps, void* stream);
 
 /*
  * Device-side sample_batch: B fresh uniform queries in [0,1)^N sorted by the first

@@ -1058,6 +1058,7 @@ extern "C" int ndg_epilogue(int n, int64_t G, int64_t Gev, int amp_mode, const f
 // ---------------------------------------------------------------------------------------------
 __global__ void adam_kernel(int n, int64_t rows, float* __restrict__ p, const float* __restrict__ g,
                             float* __restrict__ m1, float* __restrict__ m2, const uint8_t* __restrict__ row_mask,
+                            const uint8_t* __restrict__ flags, uint32_t require, uint32_t forbid,
                             float c1, float c2, float lr_mean, float lr_chol, float lr_color, float lr_amp, float b1,
                             float b2, float eps) {
     const int R = raw_floats(n), P = n_chol(n);
@@ -1066,6 +1067,7 @@ __global__ void adam_kernel(int n, int64_t rows, float* __restrict__ p, const fl
     const int64_t row = x / R;
     const int col = (int)(x - row * R);
     if (row_mask && !row_mask[row]) return;
+    if (flags && ((flags[row] & require) != require || (flags[row] & forbid))) return;
     const float lr = col < n ? lr_mean : (col < n + P ? lr_chol : (col < n + P + 3 ? lr_color : lr_amp));
     const float gv = g[x];
     const float a = __fadd_rn(__fmul_rn(b1, m1[x]), __fmul_rn(1.f - b1, gv));
@@ -1075,9 +1077,10 @@ __global__ void adam_kernel(int n, int64_t rows, float* __restrict__ p, const fl
     p[x] = __fsub_rn(p[x], __fdiv_rn(__fmul_rn(lr, __fdiv_rn(a, c1)), __fadd_rn(__fsqrt_rn(__fdiv_rn(b, c2)), eps)));
 }
 
-extern "C" int ndg_adam(int n, int64_t rows, float* params, const float* grad, float* m1, float* m2,
-                        const uint8_t* row_mask, int step, float lr_mean, float lr_chol, float lr_color, float lr_amp,
-                        float beta1, float beta2, float eps, void* stream) {
+namespace {
+int adam_launch(int n, int64_t rows, float* params, const float* grad, float* m1, float* m2, const uint8_t* row_mask,
+                const uint8_t* flags, uint32_t require, uint32_t forbid, int step, float lr_mean, float lr_chol,
+                float lr_color, float lr_amp, float beta1, float beta2, float eps, void* stream) {
     if (!ndg_supported_dims(n)) return NDG_ERR_UNSUPPORTED_DIMS;
     NDG_REQUIRE(step >= 1, "adam step counter starts at 1");
     const int64_t total = rows * raw_floats(n);
@@ -1086,7 +1089,27 @@ extern "C" int ndg_adam(int n, int64_t rows, float* params, const float* grad, f
     const float c2 = (float)(1.0 - pow((double)beta2, step));
     int threads = 256;
     adam_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
-        n, rows, params, grad, m1, m2, row_mask, c1, c2, lr_mean, lr_chol, lr_color, lr_amp, beta1, beta2, eps);
+        n, rows, params, grad, m1, m2, row_mask, flags, require, forbid, c1, c2, lr_mean, lr_chol, lr_color, lr_amp,
+        beta1, beta2, eps);
     NDG_CHECK_LAUNCH();
     return NDG_OK;
+}
+}  // namespace
+
+extern "C" int ndg_adam(int n, int64_t rows, float* params, const float* grad, float* m1, float* m2,
+                        const uint8_t* row_mask, int step, float lr_mean, float lr_chol, float lr_color, float lr_amp,
+                        float beta1, float beta2, float eps, void* stream) {
+    return adam_launch(n, rows, params, grad, m1, m2, row_mask, nullptr, 0, 0, step, lr_mean, lr_chol, lr_color,
+                       lr_amp, beta1, beta2, eps, stream);
+}
+
+// The same update with the row selection read straight from the mixture's flags (no mask tensor to build per
+// step): row r is updated iff (flags[r] & require) == require and (flags[r] & forbid) == 0.
+extern "C" int ndg_adam_flags(int n, int64_t rows, float* params, const float* grad, float* m1, float* m2,
+                              const uint8_t* flags, int require, int forbid, int step, float lr_mean, float lr_chol,
+                              float lr_color, float lr_amp, float beta1, float beta2, float eps, void* stream) {
+    NDG_REQUIRE(flags != nullptr && require >= 0 && require <= 255 && forbid >= 0 && forbid <= 255,
+                "flags pointer and 8-bit require / forbid masks");
+    return adam_launch(n, rows, params, grad, m1, m2, nullptr, flags, (uint32_t)require, (uint32_t)forbid, step,
+                       lr_mean, lr_chol, lr_color, lr_amp, beta1, beta2, eps, stream);
 }

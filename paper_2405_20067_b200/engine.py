@@ -30,7 +30,7 @@ import torch
 
 from . import kernels as K
 from .errors import InvalidParameterError, NonFiniteGradientError
-from .gmm import Mixture, n_chol, raw_width
+from .gmm import FLAG_CHILD, FLAG_FROZEN, Mixture, n_chol, raw_width
 
 _INT64_MAX = (1 << 63) - 1
 _BLOCKS = ("mean", "chol", "color", "amp")
@@ -775,14 +775,13 @@ def adam_step(mix: Mixture, grads: GradientBuffer, state, step: int, lr=(2e-3, 5
     """K9: bias-corrected Adam with per-block learning rates, applied to
     parent rows (not frozen) and live child rows. `state` = dict(m1p, m2p, m1c, m2c) float32."""
     n = mix.n_dims
-    fr = (mix.flags & 2) == 0
-    pmask = fr.to(torch.uint8).contiguous()
-    K.call("ndg_adam", n, mix.G, _p(mix.params), _p(grads.params), _p(state["m1p"]), _p(state["m2p"]), _p(pmask),
-           int(step), *[float(x) for x in lr], float(betas[0]), float(betas[1]), float(eps), _stream())
+    hyper = (int(step), *[float(x) for x in lr], float(betas[0]), float(betas[1]), float(eps), _stream())
+    # rows selected on the device from the flag bytes (parents: not frozen; children: live and not frozen)
+    K.call("ndg_adam_flags", n, mix.G, _p(mix.params), _p(grads.params), _p(state["m1p"]), _p(state["m2p"]),
+           _p(mix.flags), 0, FLAG_FROZEN, *hyper)
     if mix.children_live:
-        cmask = (((mix.flags & 1) != 0) & fr).to(torch.uint8).contiguous()
-        K.call("ndg_adam", n, mix.G, _p(mix.child), _p(grads.child), _p(state["m1c"]), _p(state["m2c"]), _p(cmask),
-               int(step), *[float(x) for x in lr], float(betas[0]), float(betas[1]), float(eps), _stream())
+        K.call("ndg_adam_flags", n, mix.G, _p(mix.child), _p(grads.child), _p(state["m1c"]), _p(state["m2c"]),
+               _p(mix.flags), FLAG_CHILD, FLAG_FROZEN, *hyper)
 
 
 def new_adam_state(mix: Mixture):

@@ -55,6 +55,7 @@ SIGNATURES = {
     "ndg_loss_f64": [_I, _I, _I, _I, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P],
     "ndg_epilogue": [_I, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "ndg_adam": [_I, _L, _P, _P, _P, _P, _P, _I, _F, _F, _F, _F, _F, _F, _F, _P],
+    "ndg_adam_flags": [_I, _L, _P, _P, _P, _P, _P, _I, _I, _I, _F, _F, _F, _F, _F, _F, _F, _P],
     "ndg_tc_records": [_I, _L, _P, _P, _P, _P, _P, _P, _P],
     "ndg_forward_tc": [_I, _L, _I, _P, _P, _P, _P, _P, _F, _L, _P, _P, _P, _P],
     "ndg_sample_workspace": [_L],
@@ -106,7 +107,7 @@ class NdgLaunchError(RuntimeError):
 # entry points that enqueue exactly one kernel of ours (bench.py reports the count as gpu_launches)
 LAUNCHING = {"ndg_prologue", "ndg_project", "ndg_tile_bounds", "ndg_cull_mask", "ndg_cull_prefilter", "ndg_scan_counts",
              "ndg_cull_compact", "ndg_forward", "ndg_forward_tc", "ndg_tc_records", "ndg_loss_finalize", "ndg_loss_rel_l2", "ndg_backward", "ndg_backward_mma",
-             "ndg_work_items", "ndg_bwd_bounds", "ndg_acc_dequant", "ndg_active_mask", "ndg_centre_records", "ndg_loss_f64", "ndg_backward_f64", "ndg_fd_f64", "ndg_nonfinite_query", "ndg_sample_batch", "ndg_shading_target", "ndg_epilogue", "ndg_adam",
+             "ndg_work_items", "ndg_bwd_bounds", "ndg_acc_dequant", "ndg_active_mask", "ndg_centre_records", "ndg_loss_f64", "ndg_backward_f64", "ndg_fd_f64", "ndg_nonfinite_query", "ndg_sample_batch", "ndg_shading_target", "ndg_epilogue", "ndg_adam", "ndg_adam_flags",
              "ndg_fp32_probe", "ndg_tf32_probe", "ndg_hmma_probe"}
 # entry points that enqueue several kernels: ndg_cull_prefilter = init, stats, hist, plan, scatter, zero,
 # pre-filtered cull and the dense cull (the plan makes one of the two paths exit at once)

@@ -324,6 +324,35 @@ def test_adam_matches_oracle(cuda):
     assert np.array_equal(mix.params.cpu().numpy(), p)
 
 
+def test_adam_rows_from_flags_frozen_and_children(cuda):
+    """adam_step selects rows on the device from the flag bytes (ndg_adam_flags): frozen parents and
+    children, and absent children, stay bit-for-bit untouched; the rest equal the oracle's Adam."""
+    ndg = _ndg()
+    om, mix, q, t = _mk(5, 100, 256, children=True)
+    rng = np.random.default_rng(1)
+    has_child = rng.random(100) < 0.5
+    frozen = rng.random(100) < 0.3
+    mix = ndg.Mixture.from_arrays(5, om.amp_mode, om.params, om.child, has_child, frozen)
+    assert mix.children_live
+    gp = rng.normal(size=mix.params.shape).astype(np.float32)
+    gc = rng.normal(size=mix.child.shape).astype(np.float32)
+    grads = ndg.alloc_gradients(mix.G, 2 * mix.G, 5, mix.device)
+    grads.params.copy_(torch.from_numpy(gp))
+    grads.child.copy_(torch.from_numpy(gc))
+    state = ndg.new_adam_state(mix)
+    p0, c0 = mix.params.cpu().numpy(), mix.child.cpu().numpy()
+    ndg.adam_step(mix, grads, state, step=1)
+    lr = O.block_lr(5)
+    z = np.zeros_like(p0)
+    p1 = O.adam_step(p0, gp, z, z, 1, lr)[0]
+    c1 = O.adam_step(c0, gc, z, z, 1, lr)[0]
+    upd_p = ~frozen
+    upd_c = has_child & ~frozen
+    got_p, got_c = mix.params.cpu().numpy(), mix.child.cpu().numpy()
+    assert np.array_equal(got_p[upd_p], p1[upd_p]) and np.array_equal(got_p[~upd_p], p0[~upd_p])
+    assert np.array_equal(got_c[upd_c], c1[upd_c]) and np.array_equal(got_c[~upd_c], c0[~upd_c])
+
+
 @pytest.mark.parametrize("sigma0,regime,want_tc", [(0.15, "R", True), (0.05, "C", True), (0.02, "C", False),
                                                     (0.005, "R", False)])
 def test_tc_forward_sharp_gaussians(cuda, sigma0, regime, want_tc):
