@@ -31,6 +31,9 @@ __host__ __device__ constexpr int srow_start(int i) {   // sum_{r<i} (r/2 + 1): 
 #define NDG_BWD_QUNROLL 1   // query-loop unroll factor; tuning builds only
 #endif
 constexpr int kQUnroll = NDG_BWD_QUNROLL;
+#ifndef NDG_BWD_SCALAR_S_MAXN
+#define NDG_BWD_SCALAR_S_MAXN 7   // S' rows as scalar FFMA up to this N, FFMA2 pairs above (A/B: r02_k7_scalar_s_small_n.txt)
+#endif
 #ifndef NDG_BWD_MINB
 #define NDG_BWD_MINB 3   // CTAs per SM the register budget is sized for (N <= 10); tuning builds only
 #endif
@@ -139,9 +142,20 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
         for (int i = 0; i < N; ++i) {
             const float ui = (i & 1) ? u2[i / 2].y : u2[i / 2].x;
 #ifndef NDG_BWD_KO_S       // knock-out build: no S' update (wrong results)
+            if constexpr (N <= NDG_BWD_SCALAR_S_MAXN) {
+                // small N: scalar FFMA rows (no padded lane); the loop is short enough that issue is not the
+                // limit (tools/kbench.py, profiles/r02_k7_instruction_forms_rejected.txt)
 #pragma unroll
-            for (int jp = 0; jp <= i / 2; ++jp)
-                Sp[srow_start(i) + jp] = __ffma2_rn(make_float2(ui, ui), z2[jp], Sp[srow_start(i) + jp]);
+                for (int j = 0; j <= i; ++j) {
+                    float2& sp = Sp[srow_start(i) + j / 2];
+                    if (j & 1) sp.y = fmaf(ui, z2[j / 2].y, sp.y);
+                    else sp.x = fmaf(ui, z2[j / 2].x, sp.x);
+                }
+            } else {
+#pragma unroll
+                for (int jp = 0; jp <= i / 2; ++jp)
+                    Sp[srow_start(i) + jp] = __ffma2_rn(make_float2(ui, ui), z2[jp], Sp[srow_start(i) + jp]);
+            }
 #endif
         }
         gA0 = fmaf(g, dp0, gA0);
