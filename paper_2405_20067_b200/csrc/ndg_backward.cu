@@ -32,7 +32,10 @@ __host__ __device__ constexpr int srow_start(int i) {   // sum_{r<i} (r/2 + 1): 
 #endif
 constexpr int kQUnroll = NDG_BWD_QUNROLL;
 #ifndef NDG_BWD_SCALAR_S_MAXN
-#define NDG_BWD_SCALAR_S_MAXN 7   // S' rows as scalar FFMA up to this N, FFMA2 pairs above (A/B: r02_k7_scalar_s_small_n.txt)
+#define NDG_BWD_SCALAR_S_MAXN 7   // S' rows as scalar FFMA up to this N, FFMA2 pairs above (A/B: r02_k7_s_update_forms.txt)
+#endif
+#ifndef NDG_BWD_DIAG_SCALAR_MINN
+#define NDG_BWD_DIAG_SCALAR_MINN 9   // from this N, even rows' diagonal S' entry as a scalar FFMA (A/B: r02_k7_s_update_forms.txt)
 #endif
 #ifndef NDG_BWD_MINB
 #define NDG_BWD_MINB 3   // CTAs per SM the register budget is sized for (N <= 10); tuning builds only
@@ -151,6 +154,13 @@ __global__ void __launch_bounds__(kBwdThreads, (N <= 10 ? NDG_BWD_MINB : 1))
                     if (j & 1) sp.y = fmaf(ui, z2[j / 2].y, sp.y);
                     else sp.x = fmaf(ui, z2[j / 2].x, sp.x);
                 }
+            } else if constexpr (N >= NDG_BWD_DIAG_SCALAR_MINN) {
+                // FFMA2 over the row's full pairs; an even row's last (diagonal) entry as one scalar FFMA
+                // instead of a padded FFMA2: same instruction count, 5 fewer lane-cycles per pair at N = 10
+#pragma unroll
+                for (int jp = 0; jp < (i + 1) / 2; ++jp)
+                    Sp[srow_start(i) + jp] = __ffma2_rn(make_float2(ui, ui), z2[jp], Sp[srow_start(i) + jp]);
+                if (!(i & 1)) Sp[srow_start(i) + i / 2].x = fmaf(ui, z2[i / 2].x, Sp[srow_start(i) + i / 2].x);
             } else {
 #pragma unroll
                 for (int jp = 0; jp <= i / 2; ++jp)
